@@ -1,0 +1,106 @@
+/*
+ * tenrec_b200 -- C ABI of the B200 randomized t-SVT / ADMM recovery path.
+ *
+ * Plain pointers and sizes only (no torch types).  All tensor pointers are
+ * DEVICE pointers to dense column-major arrays (first index fastest, the
+ * reference's convention, tenrec/core.py:1-8).  `dtype` selects the streaming
+ * precision of the large tensors: TR_F32 (float) or TR_F64 (double).  Small
+ * dense algebra always runs in fp64.  `stream` is a cudaStream_t (NULL = the
+ * legacy default stream).  Every call is asynchronous on `stream` unless noted
+ * and returns 0 on success; a nonzero code leaves a message in
+ * tr_last_error().  Workspaces are caller-owned device buffers whose size is
+ * given by the matching *_workspace() query.
+ *
+ * Each entry point below names the reference interface it replaces.
+ */
+#ifndef TENREC_B200_H
+#define TENREC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TR_F32 0
+#define TR_F64 1
+
+/* Transform kinds (tenrec/transform.py:44-80): FFT default, orthonormal DCT-II,
+ * explicit unitary-up-to-scale matrices. */
+#define TR_TRANSFORM_FFT 0
+#define TR_TRANSFORM_DCT 1
+#define TR_TRANSFORM_EXPLICIT 2
+
+/* Penalty kinds (tenrec/penalties.py, make_penalty:276-290) with parameters
+ * (p0, p1): l1 (-), firm (gamma), mcp (gamma), scad (a), lq (q),
+ * capped-lq (q, theta), log (gamma). */
+#define TR_PEN_L1 0
+#define TR_PEN_FIRM 1
+#define TR_PEN_MCP 2
+#define TR_PEN_SCAD 3
+#define TR_PEN_LQ 4
+#define TR_PEN_CAPPED_LQ 5
+#define TR_PEN_LOG 6
+
+/* Library version (major*10000 + minor*100 + patch). */
+int tr_version(void);
+
+/* Message of the last failed call on this host thread. */
+const char* tr_last_error(void);
+
+/* Device workspace bytes for tr_gnhtsvt_randomized / tr_rsthosvd_bki. */
+int64_t tr_lrta_workspace(int dtype, int order, const int64_t* dims, const int64_t* ranks,
+                          const int64_t* blocks, const int64_t* krylov);
+
+/*
+ * Randomized GNHTSVT -- replaces tenrec.sketch.gnhtsvt_randomized
+ * (tenrec/sketch.py:430-456) for a fixed-rank SketchConfig with the default
+ * processing order (0, 1): block-Krylov Tucker compression of modes 0 and 1
+ * (sketch.py:211-270), transform-domain singular value thresholding of the
+ * core with penalty.prox(tau, .) (shrink.py:76-106), re-expansion.
+ *
+ *   a, out        n1 x n2 x ... x nd tensors (dtype), out may not alias a
+ *   order, dims   d >= 3 and the d mode lengths
+ *   ranks/blocks/krylov  two entries each (modes 0 and 1)
+ *   seed          sketch seed; sketch entry (c, t) of processing step p is
+ *                 N(0,1) from Philox4x32-10 at (seed, p, c*b + t)
+ *   transform_kind, transform_mats, alphas
+ *                 for TR_TRANSFORM_EXPLICIT: device complex128 (interleaved)
+ *                 row-major matrices of the trailing modes, concatenated, and
+ *                 their host scalings alpha_i; ignored otherwise
+ *   penalty_kind, p0, p1, tau   the thresholding penalty and level
+ *   sketch0, sketch1  optional device override of the two sketch matrices
+ *                 (dtype, row-major (n2*nf) x b0 and (r0_eff*nf) x b1), used to
+ *                 replay an externally drawn Gaussian stream; NULL = Philox
+ */
+int tr_gnhtsvt_randomized(int dtype, const void* a, void* out, int order, const int64_t* dims,
+                          const int64_t* ranks, const int64_t* blocks, const int64_t* krylov,
+                          uint64_t seed, int transform_kind, const void* transform_mats,
+                          const double* alphas, int penalty_kind, double p0, double p1,
+                          double tau, const void* sketch0, const void* sketch1, void* workspace,
+                          int64_t workspace_bytes, void* stream);
+
+/*
+ * Fixed-rank Tucker compression of modes (0, 1) -- replaces
+ * tenrec.sketch.rsthosvd_bki(x, ranks, order=(0, 1), ...) (sketch.py:211-270).
+ * Outputs (device, fp64, zero-padded to the requested ranks):
+ *   f0 n1 x r0, f1 n2 x r1, core r0 x r1 x n3 x ... x nd, ranks_eff[2] (int64).
+ */
+int tr_rsthosvd_bki(int dtype, const void* a, int order, const int64_t* dims,
+                    const int64_t* ranks, const int64_t* blocks, const int64_t* krylov,
+                    uint64_t seed, const void* sketch0, const void* sketch1, double* f0,
+                    double* f1, double* core, int64_t* ranks_eff, void* workspace,
+                    int64_t workspace_bytes, void* stream);
+
+/*
+ * Elementwise proximity operator -- replaces Penalty.prox(mu, v)
+ * (tenrec/penalties.py:45-61) on a device array of n values (dtype).
+ */
+int tr_prox(int dtype, int penalty_kind, double p0, double p1, double mu, const void* v,
+            void* out, int64_t n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TENREC_B200_H */

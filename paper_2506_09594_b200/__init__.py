@@ -1,0 +1,21 @@
+"""B200-native randomized t-SVT and nonconvex tensor-recovery hot path.
+
+Drop-in for the hot path of the reference package ``tenrec``
+(/root/reference/pkg/src/tenrec): the same public names and call signatures
+for the randomized low-rank tensor approximation and the ADMM solvers, backed
+by hand-written sm_100a CUDA kernels behind the C ABI in
+``include/tenrec_b200.h``.  There is no CPU fallback.
+"""
+
+from .penalties import (PENALTY_NAMES, L1, MCP, SCAD, CappedLq, Firm, LogPenalty, Lq, Penalty,
+                        make_penalty)
+from .sketch import SketchConfig, TuckerFactors, gnhtsvt_randomized, rsthosvd_bki
+from .transform import DEFAULT_TRANSFORM, Transform, TransformError
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "PENALTY_NAMES", "L1", "MCP", "SCAD", "CappedLq", "Firm", "LogPenalty", "Lq", "Penalty",
+    "make_penalty", "SketchConfig", "TuckerFactors", "gnhtsvt_randomized", "rsthosvd_bki",
+    "DEFAULT_TRANSFORM", "Transform", "TransformError",
+]

@@ -1,0 +1,90 @@
+"""ctypes binding of the C ABI in include/tenrec_b200.h.
+
+The product path has exactly one implementation: the CUDA library built
+in-tree (``paper_2506_09594_b200/libtenrec_b200.so``).  If it is missing or a
+GPU is not visible, every compute call raises -- there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtenrec_b200.so")
+
+F32, F64 = 0, 1
+TRANSFORM_KINDS = {"fft": 0, "dct": 1, "explicit": 2}
+
+_c_i64p = ctypes.POINTER(ctypes.c_int64)
+_c_dp = ctypes.POINTER(ctypes.c_double)
+_vp = ctypes.c_void_p
+
+# name -> (restype, argtypes); the list is the contract tests check against the header
+SIGNATURES = {
+    "tr_version": (ctypes.c_int, []),
+    "tr_last_error": (ctypes.c_char_p, []),
+    "tr_lrta_workspace": (ctypes.c_int64, [ctypes.c_int, ctypes.c_int, _c_i64p, _c_i64p, _c_i64p,
+                                           _c_i64p]),
+    "tr_gnhtsvt_randomized": (ctypes.c_int, [
+        ctypes.c_int, _vp, _vp, ctypes.c_int, _c_i64p, _c_i64p, _c_i64p, _c_i64p, ctypes.c_uint64,
+        ctypes.c_int, _vp, _c_dp, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+        _vp, _vp, _vp, ctypes.c_int64, _vp]),
+    "tr_rsthosvd_bki": (ctypes.c_int, [
+        ctypes.c_int, _vp, ctypes.c_int, _c_i64p, _c_i64p, _c_i64p, _c_i64p, ctypes.c_uint64,
+        _vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int64, _vp]),
+    "tr_prox": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                               ctypes.c_double, _vp, _vp, ctypes.c_int64, _vp]),
+}
+
+_LIB = None
+
+
+class CudaPathError(RuntimeError):
+    """The B200 library is unavailable or a kernel call failed."""
+
+
+def load(path: str = LIB_PATH):
+    """Load the shared library and bind every exported symbol (no GPU needed)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(path):
+        raise CudaPathError(
+            f"{path} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _LIB = lib
+    return lib
+
+
+def lib():
+    """The library, after checking that a CUDA device is visible."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise CudaPathError("the tenrec B200 path needs a CUDA device; none is visible")
+    return load()
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        msg = _LIB.tr_last_error().decode() if _LIB is not None else "?"
+        if rc == 1:
+            raise ValueError(msg)
+        raise CudaPathError(msg)
+
+
+def i64(values):
+    arr = (ctypes.c_int64 * max(1, len(values)))(*[int(v) for v in values])
+    return arr
+
+
+def stream_ptr(stream=None):
+    import torch
+
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)

@@ -1,0 +1,432 @@
+// Host orchestration of the randomized t-SVT on one stream, and its C ABI.
+//
+// One call = one launch sequence, fully asynchronous: data-dependent ranks
+// (Krylov deflation, r_eff) stay on the device and later kernels read them,
+// so the whole LRTA can be captured into a CUDA graph by the caller.
+#include <cstdarg>
+#include <cstring>
+#include <algorithm>
+
+#include "../../include/tenrec_b200.h"
+#include "core_svt.cuh"
+#include "lrta_kernels.cuh"
+
+namespace tr {
+
+static thread_local char g_err[2048] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+// Bump allocator over the caller's workspace; base == nullptr only sizes.
+struct Carve {
+  char* base;
+  int64_t off = 0;
+  explicit Carve(void* b) : base((char*)b) {}
+  template <typename X>
+  X* take(int64_t count) {
+    off = align_up(off, 256);
+    X* p = base ? reinterpret_cast<X*>(base + off) : nullptr;
+    off += (count > 0 ? count : 1) * (int64_t)sizeof(X);
+    return p;
+  }
+};
+
+struct Shape {
+  int order;
+  int64_t n1, n2, nf;
+  Trailing tr;
+  int64_t r0, r1, b0, b1, q0, q1, s0, s1;
+};
+
+static int make_shape(int order, const int64_t* dims, const int64_t* ranks, const int64_t* blocks,
+                      const int64_t* krylov, Shape& sh) {
+  TR_REQUIRE(order >= 3 && order <= 10, "order must be in [3, 10], got %d", order);
+  sh.order = order;
+  sh.n1 = dims[0];
+  sh.n2 = dims[1];
+  sh.nf = 1;
+  sh.tr.nt = order - 2;
+  for (int i = 0; i < 8; ++i) sh.tr.d[i] = 1;
+  for (int i = 2; i < order; ++i) {
+    TR_REQUIRE(dims[i] >= 1, "mode %d has length %lld", i, (long long)dims[i]);
+    sh.nf *= dims[i];
+    sh.tr.d[i - 2] = dims[i];
+  }
+  TR_REQUIRE(sh.n1 >= 1 && sh.n2 >= 1, "empty leading modes");
+  sh.r0 = ranks[0];
+  sh.r1 = ranks[1];
+  sh.b0 = blocks[0];
+  sh.b1 = blocks[1];
+  sh.q0 = krylov[0];
+  sh.q1 = krylov[1];
+  TR_REQUIRE(sh.r0 >= 1 && sh.r0 <= sh.n1 && sh.r1 >= 1 && sh.r1 <= sh.n2,
+             "ranks (%lld, %lld) out of range", (long long)sh.r0, (long long)sh.r1);
+  TR_REQUIRE(sh.r0 <= 64 && sh.r1 <= 64, "ranks above 64 are not supported on the GPU path");
+  TR_REQUIRE(sh.b0 >= 1 && sh.b0 <= sh.r0 && sh.b1 >= 1 && sh.b1 <= sh.r1,
+             "block sizes must satisfy 1 <= b <= r");
+  TR_REQUIRE(sh.b0 <= 32 && sh.b1 <= 32, "block sizes above 32 are not supported");
+  TR_REQUIRE(sh.q0 >= 0 && sh.q1 >= 0, "Krylov depth must be >= 0");
+  TR_REQUIRE((sh.q0 + 1) * sh.b0 >= sh.r0 && (sh.q1 + 1) * sh.b1 >= sh.r1, "(q+1)*b < rank");
+  sh.s0 = (sh.q0 + 1) * sh.b0;
+  sh.s1 = (sh.q1 + 1) * sh.b1;
+  TR_REQUIRE(sh.s0 <= 64 && sh.s1 <= 64, "Krylov block width (q+1)*b above 64 is not supported");
+  return 0;
+}
+
+template <typename T>
+struct Bufs {
+  double *partial, *K, *work, *Z, *Mpart, *M;
+  T *Zt, *P, *coef, *W;
+  double *V0, *V1, *F0, *F1;
+  T *F0t, *F1t, *A1, *C1;
+  double* core;
+  cplx *cf0, *cf1, *U;
+  int64_t* info;
+  int64_t max_parts, max_mparts;
+};
+
+static int64_t rank_splits(int64_t m, int64_t n) {
+  const int64_t rowtiles = cdiv(m, 256);
+  int64_t splits = std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 4 * num_sms() / rowtiles));
+  return splits;
+}
+
+template <typename T>
+static void carve(Carve& cv, const Shape& sh, Bufs<T>& b) {
+  const int64_t mmax = std::max(sh.n1, sh.n2);
+  const int64_t smax = std::max(sh.s0, sh.s1);
+  const int64_t bmax = std::max(sh.b0, sh.b1);
+  const int64_t nA0 = sh.n2 * sh.nf, nA1 = sh.r0 * sh.nf;
+  const int64_t nmax = std::max(nA0, nA1);
+  b.max_parts = std::max(rank_splits(sh.n1, nA0), rank_splits(sh.n2, nA1));
+  b.max_mparts = std::min<int64_t>(cdiv(nmax, 64), 2 * 148);
+  b.partial = cv.take<double>(b.max_parts * mmax * bmax);
+  b.K = cv.take<double>(mmax * smax);
+  b.work = cv.take<double>(mmax * smax);
+  b.Z = cv.take<double>(mmax * smax);
+  b.Mpart = cv.take<double>(b.max_mparts * smax * smax);
+  b.M = cv.take<double>(smax * smax);
+  b.Zt = cv.take<T>(mmax * smax);
+  b.P = cv.take<T>(mmax * bmax);
+  b.coef = cv.take<T>(nmax * bmax);
+  b.W = cv.take<T>(nmax * smax);
+  b.V0 = cv.take<double>(sh.s0 * sh.r0);
+  b.V1 = cv.take<double>(sh.s1 * sh.r1);
+  b.F0 = cv.take<double>(sh.n1 * sh.r0);
+  b.F1 = cv.take<double>(sh.n2 * sh.r1);
+  b.F0t = cv.take<T>(sh.n1 * sh.r0);
+  b.F1t = cv.take<T>(sh.n2 * sh.r1);
+  b.A1 = cv.take<T>(sh.n2 * nA1);
+  b.C1 = cv.take<T>(sh.r0 * sh.n2 * sh.nf);
+  b.core = cv.take<double>(sh.r0 * sh.r1 * sh.nf);
+  b.cf0 = cv.take<cplx>(sh.r0 * sh.r1 * sh.nf);
+  b.cf1 = cv.take<cplx>(sh.r0 * sh.r1 * sh.nf);
+  int64_t usz = 0;
+  for (int i = 0; i < sh.tr.nt; ++i) usz += sh.tr.d[i] * sh.tr.d[i];
+  b.U = cv.take<cplx>(usz);
+  b.info = cv.take<int64_t>(8);
+}
+
+template <typename T, int B>
+static void launch_rank_update(const T* A, int64_t m, int64_t n, int b, const T* coef,
+                               const T* gover, SketchSpec sk, double* partial, int64_t splits,
+                               cudaStream_t st) {
+  const int64_t cps = cdiv(n, splits);
+  const int64_t sp = cdiv(n, cps);
+  dim3 grid((unsigned)cdiv(m, 256), (unsigned)sp);
+  k_rank_update<T, B><<<grid, 256, 0, st>>>(A, m, n, b, coef, gover, sk, cps, partial);
+}
+
+// partial (nparts x m x b) over the columns, dispatching the register width.
+template <typename T>
+static int64_t rank_update(const T* A, int64_t m, int64_t n, int b, const T* coef, const T* gover,
+                           SketchSpec sk, double* partial, cudaStream_t st) {
+  const int64_t splits = rank_splits(m, n);
+  const int64_t sp = cdiv(n, cdiv(n, splits));
+  if (b <= 8) launch_rank_update<T, 8>(A, m, n, b, coef, gover, sk, partial, splits, st);
+  else if (b <= 16) launch_rank_update<T, 16>(A, m, n, b, coef, gover, sk, partial, splits, st);
+  else launch_rank_update<T, 32>(A, m, n, b, coef, gover, sk, partial, splits, st);
+  return sp;
+}
+
+template <typename T>
+static void dot_cols(const T* A, int64_t m, int64_t n, const T* Z, int s, T* W, cudaStream_t st) {
+  const int64_t warps = std::min<int64_t>(n, (int64_t)num_sms() * 64);
+  const unsigned grid = (unsigned)cdiv(warps * 32, 256);
+  if (s <= 8) k_dot_cols<T, 8><<<grid, 256, 0, st>>>(A, m, n, Z, s, W);
+  else if (s <= 16) k_dot_cols<T, 16><<<grid, 256, 0, st>>>(A, m, n, Z, s, W);
+  else if (s <= 32) k_dot_cols<T, 32><<<grid, 256, 0, st>>>(A, m, n, Z, s, W);
+  else k_dot_cols<T, 64><<<grid, 256, 0, st>>>(A, m, n, Z, s, W);
+}
+
+static void reduce(const double* part, int64_t nparts, int64_t len, double* out, cudaStream_t st) {
+  k_reduce_partials<<<(unsigned)cdiv(len, 256), 256, 0, st>>>(part, (int)nparts, len, out);
+}
+
+// One mode of R-STHOSVD-BKI on the m x n unfolding A (sketch.py:243-265).
+// Leaves the factor in F (fp64) / Ft, the eigenvectors V (s x r) and
+// W = A^T Z (n x s) for the core; info[0] = s_eff, info[1] = r_eff.
+template <typename T>
+static int bki_mode(const T* A, int64_t m, int64_t n, int r, int b, int q, SketchSpec sk,
+                    const T* gover, Bufs<T>& bf, double* V, double* F, T* Ft, int64_t* info,
+                    cudaStream_t st) {
+  const int s = (q + 1) * b;
+  int64_t np = rank_update<T>(A, m, n, b, nullptr, gover, sk, bf.partial, st);
+  reduce(bf.partial, np, m * b, bf.K, st);
+  k_normalize_piece<T><<<1, 1024, 0, st>>>(bf.K, m * b, bf.P);
+  for (int k = 1; k <= q; ++k) {
+    dot_cols<T>(A, m, n, bf.P, b, bf.coef, st);
+    np = rank_update<T>(A, m, n, b, bf.coef, nullptr, sk, bf.partial, st);
+    double* slot = bf.K + m * (int64_t)b * k;
+    reduce(bf.partial, np, m * b, slot, st);
+    k_normalize_piece<T><<<1, 1024, 0, st>>>(slot, m * b, bf.P);
+  }
+  k_orth<T><<<1, 1024, 0, st>>>(bf.K, m, s, bf.work, bf.Z, bf.Zt, info);
+  dot_cols<T>(A, m, n, bf.Zt, s, bf.W, st);
+  const int64_t mparts = std::min<int64_t>(cdiv(n, 64), bf.max_mparts);
+  const int64_t rpb = cdiv(n, mparts);
+  const int64_t mp = cdiv(n, rpb);
+  k_wtw<T><<<(unsigned)mp, 256, 32 * s * sizeof(double), st>>>(bf.W, n, s, rpb, bf.Mpart);
+  reduce(bf.Mpart, mp, (int64_t)s * s, bf.M, st);
+  k_ritz<T><<<1, 256, 2 * 64 * 65 * sizeof(double), st>>>(bf.M, s, bf.Z, m, r, V, F, Ft, info);
+  TR_LAUNCH_CHECK();
+  return 0;
+}
+
+template <typename T>
+static int lrta_compress(const T* a, const Shape& sh, uint64_t seed, const T* g0, const T* g1,
+                         Bufs<T>& bf, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    TR_CUDA(cudaFuncSetAttribute(k_ritz<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 2 * 64 * 65 * (int)sizeof(double)));
+    attr = true;
+  }
+  const int64_t nA0 = sh.n2 * sh.nf, nA1 = sh.r0 * sh.nf;
+  // mode 0 on the tensor itself (m = n1, n = n2 * nf)
+  SketchSpec sk0{seed, 0, nA0, nullptr};
+  if (bki_mode<T>(a, sh.n1, nA0, (int)sh.r0, (int)sh.b0, (int)sh.q0, sk0, g0, bf, bf.V0, bf.F0,
+                  bf.F0t, bf.info, st))
+    return 2;
+  // core rows -> mode-1 unfolding (n2 x r0*nf), contiguous columns
+  k_core_from_w<T, T><<<(unsigned)cdiv(nA0 * sh.r0, 256), 256, 0, st>>>(
+      bf.W, nA0, (int)sh.s0, bf.V0, (int)sh.r0, sh.n2, bf.A1);
+  // mode 1 on the core (m = n2, n = r0 * nf); logical columns use r0_eff
+  SketchSpec sk1{seed, 1, sh.r0, bf.info + 1};
+  if (bki_mode<T>(bf.A1, sh.n2, nA1, (int)sh.r1, (int)sh.b1, (int)sh.q1, sk1, g1, bf, bf.V1,
+                  bf.F1, bf.F1t, bf.info + 2, st))
+    return 2;
+  k_core_from_w<T, double><<<(unsigned)cdiv(nA1 * sh.r1, 256), 256, 0, st>>>(
+      bf.W, nA1, (int)sh.s1, bf.V1, (int)sh.r1, sh.r0, bf.core);
+  TR_LAUNCH_CHECK();
+  return 0;
+}
+
+// Transform-domain SVT of the r0 x r1 x trailing core in place (bf.core).
+template <typename T>
+static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* alphas,
+                    Penalty pen, double tau, Bufs<T>& bf, cudaStream_t st) {
+  const int64_t face = sh.r0 * sh.r1;
+  const int nt = sh.tr.nt;
+  const cplx* U[8];
+  double al[8];
+  int64_t uoff = 0;
+  for (int i = 0; i < nt; ++i) {
+    const int n = (int)sh.tr.d[i];
+    if (kind == TR_TRANSFORM_EXPLICIT) {
+      U[i] = mats + uoff;
+      al[i] = alphas[i];
+    } else {
+      k_build_transform<<<(unsigned)cdiv((int64_t)n * n, 256), 256, 0, st>>>(kind, n, bf.U + uoff);
+      U[i] = bf.U + uoff;
+      al[i] = kind == TR_TRANSFORM_FFT ? (double)n : 1.0;
+    }
+    uoff += (int64_t)n * n;
+  }
+  const int64_t total = face * sh.nf;
+  const unsigned g = (unsigned)cdiv(total, 256);
+  // forward: mode products along trailing modes 2..d-1
+  const void* src = bf.core;
+  int src_real = 1;
+  cplx* bufs[2] = {bf.cf0, bf.cf1};
+  int cur = 0;
+  int64_t st_lo = face;
+  for (int i = 0; i < nt; ++i) {
+    const int n = (int)sh.tr.d[i];
+    const int64_t hi = sh.nf / (st_lo / face) / n;
+    k_mode_product<<<g, 256, 0, st>>>(src, src_real, bufs[cur], 0, st_lo, n, hi, U[i], 0, 1.0);
+    src = bufs[cur];
+    src_real = 0;
+    cur ^= 1;
+    st_lo *= n;
+  }
+  cplx* faces = (cplx*)src;
+  const size_t smem = (size_t)(face + sh.r1 * sh.r1) * sizeof(cplx);
+  static bool attr = false;
+  if (!attr) {
+    TR_CUDA(cudaFuncSetAttribute(k_face_svt, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 2 * 64 * 64 * (int)sizeof(cplx)));
+    attr = true;
+  }
+  k_face_svt<<<(unsigned)sh.nf, 1024, smem, st>>>(faces, (int)sh.r0, (int)sh.r1, pen, tau);
+  if (kind == TR_TRANSFORM_FFT) k_mirror_fix<<<g, 256, 0, st>>>(faces, face, sh.nf, sh.tr);
+  // inverse: U^H / alpha in reverse mode order, real part on the last step
+  for (int i = nt - 1; i >= 0; --i) {
+    const int n = (int)sh.tr.d[i];
+    st_lo /= n;
+    const int64_t hi = sh.nf / (st_lo / face) / n;
+    const bool last = (i == 0);
+    void* dst = last ? (void*)bf.core : (void*)bufs[cur];
+    k_mode_product<<<g, 256, 0, st>>>(src, 0, dst, last ? 1 : 0, st_lo, n, hi, U[i], 1, al[i]);
+    src = dst;
+    cur ^= 1;
+  }
+  TR_LAUNCH_CHECK();
+  return 0;
+}
+
+template <typename T>
+static int expand(const Shape& sh, Bufs<T>& bf, T* out, cudaStream_t st) {
+  const int64_t N = sh.n2 * sh.nf;
+  k_expand_mode1<T><<<(unsigned)cdiv(sh.r0 * N, 256), 256, 0, st>>>(
+      bf.core, (int)sh.r0, (int)sh.r1, sh.nf, bf.F1, sh.n2, bf.C1);
+  dim3 grid((unsigned)cdiv(sh.n1, 64), (unsigned)cdiv(N, 64));
+  const int smem = 2 * 64 * 65 * (int)sizeof(T);
+  static bool attr = false;
+  if (!attr) {
+    TR_CUDA(cudaFuncSetAttribute(k_gemm_expand<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem));
+    attr = true;
+  }
+  k_gemm_expand<T><<<grid, 256, smem, st>>>(bf.F0t, sh.n1, (int)sh.r0, bf.C1, N, out);
+  TR_LAUNCH_CHECK();
+  return 0;
+}
+
+template <typename T>
+static int gnhtsvt_randomized_t(const void* a, void* out, const Shape& sh, uint64_t seed,
+                                int kind, const void* mats, const double* alphas, Penalty pen,
+                                double tau, const void* g0, const void* g1, void* ws,
+                                int64_t ws_bytes, cudaStream_t st) {
+  Carve cv(ws);
+  Bufs<T> bf;
+  carve<T>(cv, sh, bf);
+  TR_REQUIRE(ws_bytes >= cv.off, "workspace too small: %lld < %lld", (long long)ws_bytes,
+             (long long)cv.off);
+  if (lrta_compress<T>((const T*)a, sh, seed, (const T*)g0, (const T*)g1, bf, st)) return 2;
+  if (core_svt<T>(sh, kind, (const cplx*)mats, alphas, pen, tau, bf, st)) return 2;
+  return expand<T>(sh, bf, (T*)out, st);
+}
+
+template <typename T>
+static int rsthosvd_t(const void* a, const Shape& sh, uint64_t seed, const void* g0,
+                      const void* g1, double* f0, double* f1, double* core, int64_t* reff,
+                      void* ws, int64_t ws_bytes, cudaStream_t st) {
+  Carve cv(ws);
+  Bufs<T> bf;
+  carve<T>(cv, sh, bf);
+  TR_REQUIRE(ws_bytes >= cv.off, "workspace too small: %lld < %lld", (long long)ws_bytes,
+             (long long)cv.off);
+  if (lrta_compress<T>((const T*)a, sh, seed, (const T*)g0, (const T*)g1, bf, st)) return 2;
+  TR_CUDA(cudaMemcpyAsync(f0, bf.F0, sizeof(double) * sh.n1 * sh.r0, cudaMemcpyDeviceToDevice, st));
+  TR_CUDA(cudaMemcpyAsync(f1, bf.F1, sizeof(double) * sh.n2 * sh.r1, cudaMemcpyDeviceToDevice, st));
+  TR_CUDA(cudaMemcpyAsync(core, bf.core, sizeof(double) * sh.r0 * sh.r1 * sh.nf,
+                          cudaMemcpyDeviceToDevice, st));
+  TR_CUDA(cudaMemcpyAsync(reff, bf.info + 1, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+  TR_CUDA(cudaMemcpyAsync(reff + 1, bf.info + 3, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+  return 0;
+}
+
+template <typename T>
+__global__ void k_prox(Penalty pen, double mu, const T* __restrict__ v, T* __restrict__ out,
+                       int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (T)prox(pen, mu, (double)v[i]);
+}
+
+}  // namespace tr
+
+using namespace tr;
+
+extern "C" {
+
+int tr_version(void) { return 100; }
+
+const char* tr_last_error(void) { return g_err; }
+
+int64_t tr_lrta_workspace(int dtype, int order, const int64_t* dims, const int64_t* ranks,
+                          const int64_t* blocks, const int64_t* krylov) {
+  Shape sh;
+  if (make_shape(order, dims, ranks, blocks, krylov, sh)) return -1;
+  Carve cv(nullptr);
+  if (dtype == TR_F32) {
+    Bufs<float> b;
+    carve<float>(cv, sh, b);
+  } else {
+    Bufs<double> b;
+    carve<double>(cv, sh, b);
+  }
+  return cv.off;
+}
+
+int tr_gnhtsvt_randomized(int dtype, const void* a, void* out, int order, const int64_t* dims,
+                          const int64_t* ranks, const int64_t* blocks, const int64_t* krylov,
+                          uint64_t seed, int transform_kind, const void* transform_mats,
+                          const double* alphas, int penalty_kind, double p0, double p1,
+                          double tau, const void* sketch0, const void* sketch1, void* workspace,
+                          int64_t workspace_bytes, void* stream) {
+  Shape sh;
+  if (make_shape(order, dims, ranks, blocks, krylov, sh)) return 1;
+  TR_REQUIRE(transform_kind >= 0 && transform_kind <= 2, "bad transform kind %d", transform_kind);
+  TR_REQUIRE(transform_kind != TR_TRANSFORM_EXPLICIT || (transform_mats && alphas),
+             "explicit transform needs matrices and alphas");
+  TR_REQUIRE(penalty_kind >= 0 && penalty_kind <= 6, "bad penalty kind %d", penalty_kind);
+  TR_REQUIRE(tau >= 0.0, "tau must be >= 0");
+  TR_REQUIRE(a && out && workspace, "null pointer argument");
+  Penalty pen{penalty_kind, p0, p1};
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == TR_F32)
+    return gnhtsvt_randomized_t<float>(a, out, sh, seed, transform_kind, transform_mats, alphas,
+                                       pen, tau, sketch0, sketch1, workspace, workspace_bytes, st);
+  TR_REQUIRE(dtype == TR_F64, "bad dtype %d", dtype);
+  return gnhtsvt_randomized_t<double>(a, out, sh, seed, transform_kind, transform_mats, alphas,
+                                      pen, tau, sketch0, sketch1, workspace, workspace_bytes, st);
+}
+
+int tr_rsthosvd_bki(int dtype, const void* a, int order, const int64_t* dims,
+                    const int64_t* ranks, const int64_t* blocks, const int64_t* krylov,
+                    uint64_t seed, const void* sketch0, const void* sketch1, double* f0,
+                    double* f1, double* core, int64_t* ranks_eff, void* workspace,
+                    int64_t workspace_bytes, void* stream) {
+  Shape sh;
+  if (make_shape(order, dims, ranks, blocks, krylov, sh)) return 1;
+  TR_REQUIRE(a && f0 && f1 && core && ranks_eff && workspace, "null pointer argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == TR_F32)
+    return rsthosvd_t<float>(a, sh, seed, sketch0, sketch1, f0, f1, core, ranks_eff, workspace,
+                             workspace_bytes, st);
+  TR_REQUIRE(dtype == TR_F64, "bad dtype %d", dtype);
+  return rsthosvd_t<double>(a, sh, seed, sketch0, sketch1, f0, f1, core, ranks_eff, workspace,
+                            workspace_bytes, st);
+}
+
+int tr_prox(int dtype, int penalty_kind, double p0, double p1, double mu, const void* v,
+            void* out, int64_t n, void* stream) {
+  TR_REQUIRE(penalty_kind >= 0 && penalty_kind <= 6, "bad penalty kind %d", penalty_kind);
+  TR_REQUIRE(mu >= 0.0, "prox level mu must be >= 0");
+  if (n <= 0) return 0;
+  Penalty pen{penalty_kind, p0, p1};
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned g = (unsigned)cdiv(n, 256);
+  if (dtype == TR_F32) k_prox<float><<<g, 256, 0, st>>>(pen, mu, (const float*)v, (float*)out, n);
+  else k_prox<double><<<g, 256, 0, st>>>(pen, mu, (const double*)v, (double*)out, n);
+  TR_LAUNCH_CHECK();
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,96 @@
+"""Host <-> device layout plumbing.
+
+The reference stores tensors column-major (first index fastest,
+tenrec/core.py:1-8) and every kernel of this package reads that layout.  A
+``ColMajor`` wraps a flat CUDA buffer plus its dims; numpy inputs are copied
+(pinned host -> HBM) in Fortran order, torch CUDA inputs are permuted once.
+Results go back in the caller's container type.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import _lib
+
+
+class ColMajor:
+    __slots__ = ("flat", "dims", "kind", "np_dtype")
+
+    def __init__(self, flat, dims, kind, np_dtype):
+        self.flat = flat
+        self.dims = tuple(int(v) for v in dims)
+        self.kind = kind  # "numpy" | "torch"
+        self.np_dtype = np_dtype
+
+    @property
+    def dtype_code(self):
+        import torch
+
+        return _lib.F32 if self.flat.dtype == torch.float32 else _lib.F64
+
+    @property
+    def ptr(self):
+        return self.flat.data_ptr()
+
+    def numel(self):
+        return int(math.prod(self.dims))
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def to_device(x, dtype=None) -> ColMajor:
+    """Column-major CUDA copy of ``x`` (numpy array, scalar list or torch tensor)."""
+    torch = _torch()
+    _lib.lib()
+    if isinstance(x, torch.Tensor):
+        if dtype is None:
+            dtype = torch.float32 if x.dtype == torch.float32 else torch.float64
+        dims = tuple(x.shape)
+        t = x.to(device="cuda", dtype=dtype)
+        flat = t.permute(*reversed(range(t.dim()))).contiguous().reshape(-1) if t.dim() else t
+        return ColMajor(flat, dims, "torch", None)
+    a = np.asarray(x)
+    if dtype is None:
+        np_dtype = np.float32 if a.dtype == np.float32 else np.float64
+    else:
+        np_dtype = np.float32 if dtype == torch.float32 else np.float64
+    a = a.astype(np_dtype, copy=False)
+    host = torch.from_numpy(np.ascontiguousarray(a.ravel(order="F")))
+    flat = host.pin_memory().to("cuda", non_blocking=True) if host.numel() else host.to("cuda")
+    return ColMajor(flat, a.shape, "numpy", np_dtype)
+
+
+def empty_like(cm: ColMajor, dims=None) -> ColMajor:
+    torch = _torch()
+    dims = cm.dims if dims is None else tuple(dims)
+    flat = torch.empty(int(math.prod(dims)), dtype=cm.flat.dtype, device="cuda")
+    return ColMajor(flat, dims, cm.kind, cm.np_dtype)
+
+
+def from_device(cm: ColMajor):
+    """Back to the caller's container: numpy (same dtype) or a CUDA tensor view."""
+    if cm.kind == "numpy":
+        return cm.flat.cpu().numpy().reshape(cm.dims, order="F")
+    d = len(cm.dims)
+    return cm.flat.reshape(tuple(reversed(cm.dims))).permute(*reversed(range(d)))
+
+
+_WORKSPACES = {}
+
+
+def workspace(nbytes: int):
+    """Cached device workspace of at least ``nbytes`` (per device)."""
+    torch = _torch()
+    dev = torch.cuda.current_device()
+    buf = _WORKSPACES.get(dev)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device="cuda")
+        _WORKSPACES[dev] = buf
+    return buf
