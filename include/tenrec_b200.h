@@ -99,6 +99,19 @@ int tr_rsthosvd_bki(int dtype, const void* a, int order, const int64_t* dims,
 int tr_prox(int dtype, int penalty_kind, double p0, double p1, double mu, const void* v,
             void* out, int64_t n, void* stream);
 
+/* Number of kernels this library has launched in the process (accounting). */
+int64_t tr_launch_count(void);
+
+/* Enable (1) / disable (0) per-category CUDA-event timing of every launch;
+ * either call discards previously recorded events. */
+int tr_profile_enable(int on);
+
+/* Synchronise the recorded events and aggregate them per kernel category:
+ * writes up to max_entries totals (ms) and launch counts, and the category
+ * names joined by '\n' into `names`.  Returns the number of categories. */
+int tr_profile_read(char* names, int64_t names_len, double* ms, int64_t* counts,
+                    int max_entries);
+
 #ifdef __cplusplus
 }
 #endif

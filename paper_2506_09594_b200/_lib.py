@@ -33,6 +33,10 @@ SIGNATURES = {
     "tr_rsthosvd_bki": (ctypes.c_int, [
         ctypes.c_int, _vp, ctypes.c_int, _c_i64p, _c_i64p, _c_i64p, _c_i64p, ctypes.c_uint64,
         _vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int64, _vp]),
+    "tr_launch_count": (ctypes.c_int64, []),
+    "tr_profile_enable": (ctypes.c_int, [ctypes.c_int]),
+    "tr_profile_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int64, _c_dp, _c_i64p,
+                                       ctypes.c_int]),
     "tr_prox": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double,
                                ctypes.c_double, _vp, _vp, ctypes.c_int64, _vp]),
 }
@@ -88,3 +92,16 @@ def stream_ptr(stream=None):
 
     s = torch.cuda.current_stream() if stream is None else stream
     return ctypes.c_void_p(s.cuda_stream)
+
+
+def profile_read(max_entries: int = 64) -> dict:
+    """{category: (total_ms, launches)} of the events recorded since enable."""
+    lib = load()
+    names = ctypes.create_string_buffer(8192)
+    ms = (ctypes.c_double * max_entries)()
+    cnt = (ctypes.c_int64 * max_entries)()
+    n = lib.tr_profile_read(names, 8192, ms, cnt, max_entries)
+    if n < 0:
+        check(2)
+    cats = names.value.decode().split("\n")[:n]
+    return {c: (ms[i], cnt[i]) for i, c in enumerate(cats)}

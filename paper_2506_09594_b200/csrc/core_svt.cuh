@@ -87,6 +87,10 @@ __global__ void __launch_bounds__(1024) k_face_svt(cplx* __restrict__ faces, int
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
+  __shared__ double fred[32];
+  double f2 = 0.0;
+  for (int e = threadIdx.x; e < r0 * r1; e += blockDim.x) f2 += X[e].re * X[e].re + X[e].im * X[e].im;
+  const double fnorm2 = block_sum(f2, fred);
   const int ne = r1 + (r1 & 1);
   const int npairs = ne / 2;
   for (int sweep = 0; sweep < 60 && ne >= 2; ++sweep) {
@@ -110,7 +114,8 @@ __global__ void __launch_bounds__(1024) k_face_svt(cplx* __restrict__ faces, int
         gr = warp_sum(gr);
         gi = warp_sum(gi);
         const double g = sqrt(gr * gr + gi * gi);
-        if (!(g > 1e-15 * sqrt(al * be)) || g < 1e-300) continue;
+        // decoupled to working precision relative to the pair and to the face
+        if (!(g > 1e-15 * sqrt(al * be)) || !(g > 1e-17 * fnorm2)) continue;
         const double zeta = (be - al) / (2.0 * g);
         const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
         const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;

@@ -10,10 +10,19 @@
 #include "../../include/tenrec_b200.h"
 #include "core_svt.cuh"
 #include "lrta_kernels.cuh"
+#include "tsqr.cuh"
+#include "jacobi.cuh"
+#include "panel.cuh"
+#include "proj_tc.cuh"
+#include "prof.cuh"
 
 namespace tr {
 
 static thread_local char g_err[2048] = "";
+
+// Warp-register Jacobi (jacobi.cuh) for the small SVDs; off by default: on
+// B200 it is issue-latency bound (one warp per matrix, ~4.7 cycles/issue).
+static bool g_use_warp_jacobi = getenv("TR_WARP_JACOBI") != nullptr;
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -87,6 +96,8 @@ struct Bufs {
   double* core;
   cplx *cf0, *cf1, *U;
   int64_t* info;
+  double *tq_tau, *tq_R, *tq_C;
+  float *zhi, *zlo;
   int64_t max_parts, max_mparts;
 };
 
@@ -103,7 +114,8 @@ static void carve(Carve& cv, const Shape& sh, Bufs<T>& b) {
   const int64_t bmax = std::max(sh.b0, sh.b1);
   const int64_t nA0 = sh.n2 * sh.nf, nA1 = sh.r0 * sh.nf;
   const int64_t nmax = std::max(nA0, nA1);
-  b.max_parts = std::max(rank_splits(sh.n1, nA0), rank_splits(sh.n2, nA1));
+  b.max_parts = std::max<int64_t>(std::max(rank_splits(sh.n1, nA0), rank_splits(sh.n2, nA1)),
+                                  num_sms());
   b.max_mparts = std::min<int64_t>(cdiv(nmax, 64), 2 * 148);
   b.partial = cv.take<double>(b.max_parts * mmax * bmax);
   b.K = cv.take<double>(mmax * smax);
@@ -130,6 +142,15 @@ static void carve(Carve& cv, const Shape& sh, Bufs<T>& b) {
   for (int i = 0; i < sh.tr.nt; ++i) usz += sh.tr.d[i] * sh.tr.d[i];
   b.U = cv.take<cplx>(usz);
   b.info = cv.take<int64_t>(8);
+  int64_t tq = 0;
+  for (int64_t mm : {sh.n1, sh.n2})
+    for (int64_t ss : {sh.s0, sh.s1}) tq = std::max<int64_t>(tq, cdiv(mm, std::max<int64_t>(ss, 1)) + 1);
+  const int64_t tq_rows = tq * smax;  // nb * s bound (RB >= s)
+  b.tq_tau = cv.take<double>(tq_rows);
+  b.tq_R = cv.take<double>(tq_rows * smax);
+  b.tq_C = cv.take<double>(tq_rows * smax);
+  b.zhi = cv.take<float>(mmax * 32);
+  b.zlo = cv.take<float>(mmax * 32);
 }
 
 template <typename T, int B>
@@ -139,7 +160,7 @@ static void launch_rank_update(const T* A, int64_t m, int64_t n, int b, const T*
   const int64_t cps = cdiv(n, splits);
   const int64_t sp = cdiv(n, cps);
   dim3 grid((unsigned)cdiv(m, 256), (unsigned)sp);
-  k_rank_update<T, B><<<grid, 256, 0, st>>>(A, m, n, b, coef, gover, sk, cps, partial);
+  launch("rank_update", k_rank_update<T, B>, grid, 256, 0, st, A, m, n, b, coef, gover, sk, cps, partial);
 }
 
 // partial (nparts x m x b) over the columns, dispatching the register width.
@@ -158,14 +179,126 @@ template <typename T>
 static void dot_cols(const T* A, int64_t m, int64_t n, const T* Z, int s, T* W, cudaStream_t st) {
   const int64_t warps = std::min<int64_t>(n, (int64_t)num_sms() * 64);
   const unsigned grid = (unsigned)cdiv(warps * 32, 256);
-  if (s <= 8) k_dot_cols<T, 8><<<grid, 256, 0, st>>>(A, m, n, Z, s, W);
-  else if (s <= 16) k_dot_cols<T, 16><<<grid, 256, 0, st>>>(A, m, n, Z, s, W);
-  else if (s <= 32) k_dot_cols<T, 32><<<grid, 256, 0, st>>>(A, m, n, Z, s, W);
-  else k_dot_cols<T, 64><<<grid, 256, 0, st>>>(A, m, n, Z, s, W);
+  if (s <= 8) launch("dot_cols", k_dot_cols<T, 8>, grid, 256, 0, st, A, m, n, Z, s, W);
+  else if (s <= 16) launch("dot_cols", k_dot_cols<T, 16>, grid, 256, 0, st, A, m, n, Z, s, W);
+  else if (s <= 32) launch("dot_cols", k_dot_cols<T, 32>, grid, 256, 0, st, A, m, n, Z, s, W);
+  else launch("dot_cols", k_dot_cols<T, 64>, grid, 256, 0, st, A, m, n, Z, s, W);
+}
+
+// Fused TMA-staged panel pass (panel.cuh) when the unfolding suits it:
+// 16-byte aligned columns, m <= 2048 rows, b <= 16.
+template <typename T>
+static bool panel_ok(const T* A, int64_t m, int b) {
+  return (m * (int64_t)sizeof(T)) % 16 == 0 && m <= 2048 && b <= 16 &&
+         ((uintptr_t)A % 16) == 0 && getenv("TR_NO_PANEL") == nullptr;
+}
+
+template <typename T, int B, int Q, int MODE>
+static int64_t panel_launch(const T* A, const T* P, const T* gover, PanelArgs pa,
+                            double* partial, cudaStream_t st) {
+  const int64_t grid = std::min<int64_t>(pa.nchunks, num_sms());
+  const size_t smem = ((size_t)kPanelStages * pa.m * pa.cc + (size_t)pa.cc * B * 9) * sizeof(T);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_panel<T, B, Q, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         220 * 1024);
+    attr = true;
+  }
+  launch(MODE ? "panel_gram" : "panel_sketch", k_panel<T, B, Q, MODE>, (unsigned)grid,
+         kPanelThreads, smem, st, A, P, gover, pa, partial);
+  return grid;
+}
+
+template <typename T, int MODE>
+static int64_t panel(const T* A, int64_t m, int64_t n, int b, const T* P, const T* gover,
+                     SketchSpec sk, double* partial, cudaStream_t st) {
+  PanelArgs pa;
+  pa.m = m;
+  pa.n = n;
+  pa.b = b;
+  pa.cc = (int)std::max<int64_t>(1, std::min<int64_t>(32, (48 * 1024) / (m * (int64_t)sizeof(T))));
+  pa.nchunks = cdiv(n, pa.cc);
+  pa.sk = sk;
+  const bool q2 = m > 1024;
+  if (b <= 8)
+    return q2 ? panel_launch<T, 8, 2, MODE>(A, P, gover, pa, partial, st)
+              : panel_launch<T, 8, 1, MODE>(A, P, gover, pa, partial, st);
+  return q2 ? panel_launch<T, 16, 2, MODE>(A, P, gover, pa, partial, st)
+            : panel_launch<T, 16, 1, MODE>(A, P, gover, pa, partial, st);
 }
 
 static void reduce(const double* part, int64_t nparts, int64_t len, double* out, cudaStream_t st) {
-  k_reduce_partials<<<(unsigned)cdiv(len, 256), 256, 0, st>>>(part, (int)nparts, len, out);
+  launch("reduce_partials", k_reduce_partials, (unsigned)cdiv(len, 256), 256, 0, st, part, (int)nparts, len, out);
+}
+
+// TSQR row-block size for an m x s Krylov block and the shared memory of each
+// stage; ok = false when the blocks do not fit (single-CTA fallback).
+struct TsqrPlan {
+  bool ok;
+  int RB, nb;
+  size_t sm_local, sm_top, sm_form;
+};
+
+static TsqrPlan tsqr_plan(int64_t m, int s) {
+  TsqrPlan p{};
+  const int64_t cap = 200 * 1024;
+  int64_t rb = std::min<int64_t>(256, (cap / 8 / s - 1) / 2);
+  rb = std::max<int64_t>(rb, s);
+  p.RB = (int)rb;
+  p.nb = (int)cdiv(m, rb);
+  const int64_t nrows = (int64_t)p.nb * s;
+  p.sm_local = (size_t)((rb + 1) * s + s) * 8;
+  p.sm_form = (size_t)(2 * (rb + 1) * s + s) * 8;
+  p.sm_top = (size_t)(2 * (nrows + 1) * s + (s + 1) * s + 3 * s) * 8;
+  p.ok = (int64_t)p.sm_form <= cap && (int64_t)p.sm_top <= cap && (int64_t)p.sm_local <= cap;
+  return p;
+}
+
+template <typename T>
+static void orth_basis(int64_t m, int s, Bufs<T>& bf, int64_t* info, cudaStream_t st) {
+  const TsqrPlan p = tsqr_plan(m, s);
+  if (!p.ok) {
+    launch("orth", k_orth<T>, 1, 1024, 0, st, bf.K, m, s, bf.work, bf.Z, bf.Zt, info);
+    return;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_tsqr_local, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_tsqr_top, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_tsqr_form<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  const int64_t nrows = (int64_t)p.nb * s;
+  launch("orth", k_tsqr_local, p.nb, 1024, p.sm_local, st, bf.K, m, s, p.RB, bf.work, bf.tq_tau,
+         bf.tq_R, nrows);
+  launch("orth", k_tsqr_top, 1, 1024, p.sm_top, st, bf.tq_R, (int)nrows, s, bf.tq_C, info);
+  launch("orth", k_tsqr_form<T>, p.nb, 1024, p.sm_form, st, bf.work, bf.tq_tau, bf.tq_C,
+         (int)nrows, m, s, p.RB, bf.Z, bf.Zt);
+}
+
+// W = A^T Z and M = W^T W on the tensor cores (proj_tc.cuh) for fp32
+// unfoldings with m % 32 == 0 and s <= 32; returns false to use the generic path.
+static bool project(const float* A, int64_t m, int64_t n, int s, Bufs<float>& bf, cudaStream_t st) {
+  if (m % 32 != 0 || s > 32 || ((uintptr_t)A % 16) != 0 || getenv("TR_NO_TC") != nullptr)
+    return false;
+  launch("proj_split", k_split_z, (unsigned)cdiv(m * 32, 256), 256, 0, st, bf.Z, m, s, bf.zhi,
+         bf.zlo);
+  const int64_t ntiles = cdiv(n, 128);
+  const int64_t grid = std::min<int64_t>(ntiles, num_sms());
+  const size_t smem = (size_t)kPjStages * kPjStageBytes + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_proj_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  launch("proj_tc", k_proj_tc, (unsigned)grid, kPjThreads, smem, st, A, m, n, bf.zhi, bf.zlo, s,
+         bf.W, bf.Mpart);
+  reduce(bf.Mpart, grid, (int64_t)s * s, bf.M, st);
+  return true;
+}
+
+static bool project(const double*, int64_t, int64_t, int, Bufs<double>&, cudaStream_t) {
+  return false;
 }
 
 // One mode of R-STHOSVD-BKI on the m x n unfolding A (sketch.py:243-265).
@@ -176,24 +309,44 @@ static int bki_mode(const T* A, int64_t m, int64_t n, int r, int b, int q, Sketc
                     const T* gover, Bufs<T>& bf, double* V, double* F, T* Ft, int64_t* info,
                     cudaStream_t st) {
   const int s = (q + 1) * b;
-  int64_t np = rank_update<T>(A, m, n, b, nullptr, gover, sk, bf.partial, st);
+  const bool fused = panel_ok<T>(A, m, b);
+  int64_t np = fused ? panel<T, 0>(A, m, n, b, nullptr, gover, sk, bf.partial, st)
+                     : rank_update<T>(A, m, n, b, nullptr, gover, sk, bf.partial, st);
   reduce(bf.partial, np, m * b, bf.K, st);
-  k_normalize_piece<T><<<1, 1024, 0, st>>>(bf.K, m * b, bf.P);
+  launch("normalize_piece", k_normalize_piece<T>, 1, 1024, 0, st, bf.K, m * b, bf.P);
   for (int k = 1; k <= q; ++k) {
-    dot_cols<T>(A, m, n, bf.P, b, bf.coef, st);
-    np = rank_update<T>(A, m, n, b, bf.coef, nullptr, sk, bf.partial, st);
+    if (fused) {
+      np = panel<T, 1>(A, m, n, b, bf.P, nullptr, sk, bf.partial, st);
+    } else {
+      dot_cols<T>(A, m, n, bf.P, b, bf.coef, st);
+      np = rank_update<T>(A, m, n, b, bf.coef, nullptr, sk, bf.partial, st);
+    }
     double* slot = bf.K + m * (int64_t)b * k;
     reduce(bf.partial, np, m * b, slot, st);
-    k_normalize_piece<T><<<1, 1024, 0, st>>>(slot, m * b, bf.P);
+    launch("normalize_piece", k_normalize_piece<T>, 1, 1024, 0, st, slot, m * b, bf.P);
   }
-  k_orth<T><<<1, 1024, 0, st>>>(bf.K, m, s, bf.work, bf.Z, bf.Zt, info);
-  dot_cols<T>(A, m, n, bf.Zt, s, bf.W, st);
-  const int64_t mparts = std::min<int64_t>(cdiv(n, 64), bf.max_mparts);
-  const int64_t rpb = cdiv(n, mparts);
-  const int64_t mp = cdiv(n, rpb);
-  k_wtw<T><<<(unsigned)mp, 256, 32 * s * sizeof(double), st>>>(bf.W, n, s, rpb, bf.Mpart);
-  reduce(bf.Mpart, mp, (int64_t)s * s, bf.M, st);
-  k_ritz<T><<<1, 256, 2 * 64 * 65 * sizeof(double), st>>>(bf.M, s, bf.Z, m, r, V, F, Ft, info);
+  orth_basis<T>(m, s, bf, info, st);
+  if (!project(A, m, n, s, bf, st)) {
+    dot_cols<T>(A, m, n, bf.Zt, s, bf.W, st);
+    const int64_t mparts = std::min<int64_t>(cdiv(n, 64), bf.max_mparts);
+    const int64_t rpb = cdiv(n, mparts);
+    const int64_t mp = cdiv(n, rpb);
+    launch("wtw", k_wtw<T>, (unsigned)mp, 256, 32 * s * sizeof(double), st, bf.W, n, s, rpb,
+           bf.Mpart);
+    reduce(bf.Mpart, mp, (int64_t)s * s, bf.M, st);
+  }
+  if (s <= kJW && g_use_warp_jacobi) {
+    const size_t sm = 4 * kJW * kVld * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_ritz_warp<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      attr = true;
+    }
+    launch("ritz", k_ritz_warp<T>, 1, 256, sm, st, bf.M, s, bf.Z, m, r, V, F, Ft, info);
+  } else {
+    launch("ritz", k_ritz<T>, 1, 1024, 2 * 64 * 65 * sizeof(double), st, bf.M, s, bf.Z, m, r, V,
+           F, Ft, info);
+  }
   TR_LAUNCH_CHECK();
   return 0;
 }
@@ -214,14 +367,14 @@ static int lrta_compress(const T* a, const Shape& sh, uint64_t seed, const T* g0
                   bf.F0t, bf.info, st))
     return 2;
   // core rows -> mode-1 unfolding (n2 x r0*nf), contiguous columns
-  k_core_from_w<T, T><<<(unsigned)cdiv(nA0 * sh.r0, 256), 256, 0, st>>>(
+  launch("core_from_w", k_core_from_w<T, T>, (unsigned)cdiv(nA0 * sh.r0, 256), 256, 0, st, 
       bf.W, nA0, (int)sh.s0, bf.V0, (int)sh.r0, sh.n2, bf.A1);
   // mode 1 on the core (m = n2, n = r0 * nf); logical columns use r0_eff
   SketchSpec sk1{seed, 1, sh.r0, bf.info + 1};
   if (bki_mode<T>(bf.A1, sh.n2, nA1, (int)sh.r1, (int)sh.b1, (int)sh.q1, sk1, g1, bf, bf.V1,
                   bf.F1, bf.F1t, bf.info + 2, st))
     return 2;
-  k_core_from_w<T, double><<<(unsigned)cdiv(nA1 * sh.r1, 256), 256, 0, st>>>(
+  launch("core_from_w", k_core_from_w<T, double>, (unsigned)cdiv(nA1 * sh.r1, 256), 256, 0, st, 
       bf.W, nA1, (int)sh.s1, bf.V1, (int)sh.r1, sh.r0, bf.core);
   TR_LAUNCH_CHECK();
   return 0;
@@ -242,7 +395,7 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
       U[i] = mats + uoff;
       al[i] = alphas[i];
     } else {
-      k_build_transform<<<(unsigned)cdiv((int64_t)n * n, 256), 256, 0, st>>>(kind, n, bf.U + uoff);
+      launch("build_transform", k_build_transform, (unsigned)cdiv((int64_t)n * n, 256), 256, 0, st, kind, n, bf.U + uoff);
       U[i] = bf.U + uoff;
       al[i] = kind == TR_TRANSFORM_FFT ? (double)n : 1.0;
     }
@@ -259,7 +412,7 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
   for (int i = 0; i < nt; ++i) {
     const int n = (int)sh.tr.d[i];
     const int64_t hi = sh.nf / (st_lo / face) / n;
-    k_mode_product<<<g, 256, 0, st>>>(src, src_real, bufs[cur], 0, st_lo, n, hi, U[i], 0, 1.0);
+    launch("mode_product", k_mode_product, g, 256, 0, st, src, src_real, bufs[cur], 0, st_lo, n, hi, U[i], 0, 1.0);
     src = bufs[cur];
     src_real = 0;
     cur ^= 1;
@@ -273,8 +426,21 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
                                  2 * 64 * 64 * (int)sizeof(cplx)));
     attr = true;
   }
-  k_face_svt<<<(unsigned)sh.nf, 1024, smem, st>>>(faces, (int)sh.r0, (int)sh.r1, pen, tau);
-  if (kind == TR_TRANSFORM_FFT) k_mirror_fix<<<g, 256, 0, st>>>(faces, face, sh.nf, sh.tr);
+  if (sh.r0 <= kJW && sh.r1 <= kJW && g_use_warp_jacobi) {
+    const size_t sm = 4 * 4 * kJW * kVld * sizeof(double);
+    static bool wattr = false;
+    if (!wattr) {
+      TR_CUDA(cudaFuncSetAttribute(k_face_svt_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)sm));
+      wattr = true;
+    }
+    launch("face_svt", k_face_svt_warp, (unsigned)cdiv(sh.nf, 4), 128, sm, st, (double2*)faces,
+           (int)sh.r0, (int)sh.r1, sh.nf, pen, tau);
+  } else {
+    launch("face_svt", k_face_svt, (unsigned)sh.nf, 1024, smem, st, faces, (int)sh.r0,
+           (int)sh.r1, pen, tau);
+  }
+  if (kind == TR_TRANSFORM_FFT) launch("mirror_fix", k_mirror_fix, g, 256, 0, st, faces, face, sh.nf, sh.tr);
   // inverse: U^H / alpha in reverse mode order, real part on the last step
   for (int i = nt - 1; i >= 0; --i) {
     const int n = (int)sh.tr.d[i];
@@ -282,7 +448,7 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
     const int64_t hi = sh.nf / (st_lo / face) / n;
     const bool last = (i == 0);
     void* dst = last ? (void*)bf.core : (void*)bufs[cur];
-    k_mode_product<<<g, 256, 0, st>>>(src, 0, dst, last ? 1 : 0, st_lo, n, hi, U[i], 1, al[i]);
+    launch("mode_product", k_mode_product, g, 256, 0, st, src, 0, dst, last ? 1 : 0, st_lo, n, hi, U[i], 1, al[i]);
     src = dst;
     cur ^= 1;
   }
@@ -293,7 +459,7 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
 template <typename T>
 static int expand(const Shape& sh, Bufs<T>& bf, T* out, cudaStream_t st) {
   const int64_t N = sh.n2 * sh.nf;
-  k_expand_mode1<T><<<(unsigned)cdiv(sh.r0 * N, 256), 256, 0, st>>>(
+  launch("expand_mode1", k_expand_mode1<T>, (unsigned)cdiv(sh.r0 * N, 256), 256, 0, st, 
       bf.core, (int)sh.r0, (int)sh.r1, sh.nf, bf.F1, sh.n2, bf.C1);
   dim3 grid((unsigned)cdiv(sh.n1, 64), (unsigned)cdiv(N, 64));
   const int smem = 2 * 64 * 65 * (int)sizeof(T);
@@ -303,7 +469,7 @@ static int expand(const Shape& sh, Bufs<T>& bf, T* out, cudaStream_t st) {
                                  smem));
     attr = true;
   }
-  k_gemm_expand<T><<<grid, 256, smem, st>>>(bf.F0t, sh.n1, (int)sh.r0, bf.C1, N, out);
+  launch("gemm_expand", k_gemm_expand<T>, grid, 256, smem, st, bf.F0t, sh.n1, (int)sh.r0, bf.C1, N, out);
   TR_LAUNCH_CHECK();
   return 0;
 }
@@ -423,10 +589,70 @@ int tr_prox(int dtype, int penalty_kind, double p0, double p1, double mu, const 
   Penalty pen{penalty_kind, p0, p1};
   cudaStream_t st = (cudaStream_t)stream;
   const unsigned g = (unsigned)cdiv(n, 256);
-  if (dtype == TR_F32) k_prox<float><<<g, 256, 0, st>>>(pen, mu, (const float*)v, (float*)out, n);
-  else k_prox<double><<<g, 256, 0, st>>>(pen, mu, (const double*)v, (double*)out, n);
+  if (dtype == TR_F32) launch("prox", k_prox<float>, g, 256, 0, st, pen, mu, (const float*)v, (float*)out, n);
+  else launch("prox", k_prox<double>, g, 256, 0, st, pen, mu, (const double*)v, (double*)out, n);
   TR_LAUNCH_CHECK();
   return 0;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// launch accounting / profiling (used by bench.py)
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int64_t tr_launch_count(void) { return (int64_t)tr::profiler().launches.load(); }
+
+int tr_profile_enable(int on) {
+  tr::Profiler& p = tr::profiler();
+  std::lock_guard<std::mutex> g(p.mu);
+  for (auto& r : p.records) {
+    p.pool.push_back(r.a);
+    p.pool.push_back(r.b);
+  }
+  p.records.clear();
+  p.enabled = on != 0;
+  return 0;
+}
+
+int tr_profile_read(char* names, int64_t names_len, double* ms, int64_t* counts,
+                    int max_entries) {
+  tr::Profiler& p = tr::profiler();
+  std::lock_guard<std::mutex> g(p.mu);
+  std::vector<std::string> cats;
+  std::vector<double> tot;
+  std::vector<int64_t> cnt;
+  for (auto& r : p.records) {
+    TR_CUDA(cudaEventSynchronize(r.b));
+    float t = 0.f;
+    TR_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    size_t i = 0;
+    while (i < cats.size() && cats[i] != r.cat) ++i;
+    if (i == cats.size()) {
+      cats.emplace_back(r.cat);
+      tot.push_back(0.0);
+      cnt.push_back(0);
+    }
+    tot[i] += t;
+    cnt[i] += 1;
+    p.pool.push_back(r.a);
+    p.pool.push_back(r.b);
+  }
+  p.records.clear();
+  std::string joined;
+  int n = 0;
+  for (size_t i = 0; i < cats.size() && n < max_entries; ++i, ++n) {
+    ms[n] = tot[i];
+    counts[n] = cnt[i];
+    joined += cats[i];
+    joined += '\n';
+  }
+  if (names && names_len > 0) {
+    strncpy(names, joined.c_str(), (size_t)names_len - 1);
+    names[names_len - 1] = 0;
+  }
+  return n;
 }
 
 }  // extern "C"

@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(1024) k_orth(const double* __restrict__ K, int
 // cyclic Jacobi, descending order, F = Z V; then the canonical sign (largest
 // |entry| of every factor column positive, first index on ties).
 template <typename T>
-__global__ void __launch_bounds__(256) k_ritz(const double* __restrict__ Mfull, int s,
+__global__ void __launch_bounds__(1024) k_ritz(const double* __restrict__ Mfull, int s,
                                               const double* __restrict__ Z, int64_t m, int r,
                                               double* __restrict__ V, double* __restrict__ F,
                                               T* __restrict__ Ft, int64_t* __restrict__ info) {
@@ -285,7 +285,8 @@ __global__ void __launch_bounds__(256) k_ritz(const double* __restrict__ Mfull, 
   __shared__ double evals[64];
   __shared__ int order[64];
   __shared__ double sgn[64];
-  __shared__ double off_s;
+  __shared__ int rot_any;
+  if (threadIdx.x == 0) rot_any = 0;
   __shared__ double red[32];
   const int n = (int)info[0];  // s_eff
   const int ld = 65;
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(256) k_ritz(const double* __restrict__ Mfull, 
     const int a = i % n, b = i / n;
     if (a != b) diag2 += A[a + ld * b] * A[a + ld * b];
   }
-  const double fro2 = block_sum(diag2, red);
+  const double mnorm = sqrt(block_sum(diag2, red));
   for (int sweep = 0; sweep < 40 && ne >= 2; ++sweep) {
     for (int rnd = 0; rnd < ne - 1; ++rnd) {
       const int npairs = ne / 2;
@@ -313,7 +314,10 @@ __global__ void __launch_bounds__(256) k_ritz(const double* __restrict__ Mfull, 
         if (q < n) {
           const double apq = A[p + ld * q];
           const double app = A[p + ld * p], aqq = A[q + ld * q];
-          if (fabs(apq) > 1e-300 && fabs(apq) > 1e-18 * sqrt(fabs(app * aqq))) {
+          // skip pairs already decoupled to working precision, relative to the
+          // pair and to ||M|| (rotating rounding noise never converges)
+          if (fabs(apq) > 1e-15 * sqrt(fabs(app * aqq)) && fabs(apq) > 1e-16 * mnorm) {
+            rot_any = 1;
             const double tau = (aqq - app) / (2.0 * apq);
             const double t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
             c = 1.0 / sqrt(1.0 + t * t);
@@ -354,15 +358,13 @@ __global__ void __launch_bounds__(256) k_ritz(const double* __restrict__ Mfull, 
       }
       __syncthreads();
     }
-    double off = 0.0;
-    for (int i = threadIdx.x; i < n * n; i += blockDim.x) {
-      const int a = i % n, b = i / n;
-      if (a != b) off += A[a + ld * b] * A[a + ld * b];
-    }
-    off = block_sum(off, red);
-    if (threadIdx.x == 0) off_s = off;
+    // converged once a whole sweep needed no rotation (every |a_pq| is below
+    // 1e-15 sqrt(|a_pp a_qq|), the classical Jacobi stopping rule)
+    const int any = rot_any;
     __syncthreads();
-    if (off_s <= 1e-30 * fro2) break;
+    if (threadIdx.x == 0) rot_any = 0;
+    __syncthreads();
+    if (!any) break;
   }
   // descending order (stable on ties, like reversing eigh's ascending output)
   if (threadIdx.x == 0) {
@@ -382,47 +384,46 @@ __global__ void __launch_bounds__(256) k_ritz(const double* __restrict__ Mfull, 
   }
   __syncthreads();
   const int re = min(r, n);
-  // F = Z V (m x r), canonical sign per column
-  for (int k = 0; k < r; ++k) {
-    double best = -1.0, bval = 0.0;
-    int64_t bidx = INT64_MAX;
-    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
-      double f = 0.0;
-      if (k < re) {
-        const int col = order[k];
-        for (int j = 0; j < n; ++j) f += Z[i + m * j] * Q[j + ld * col];
-      }
-      F[i + m * k] = f;
-      const double af = fabs(f);
-      if (af > best) {
-        best = af;
-        bval = f;
-        bidx = i;
-      }
+  // F = Z V (m x r)
+  for (int64_t e = threadIdx.x; e < m * r; e += blockDim.x) {
+    const int64_t i = e % m;
+    const int k = (int)(e / m);
+    double f = 0.0;
+    if (k < re) {
+      const int col = order[k];
+      for (int j = 0; j < n; ++j) f += Z[i + m * j] * Q[j + ld * col];
     }
-    // block argmax with first-index tie break
-    __shared__ double bv_s[256];
-    __shared__ double bf_s[256];
-    __shared__ int64_t bi_s[256];
-    bv_s[threadIdx.x] = best;
-    bf_s[threadIdx.x] = bval;
-    bi_s[threadIdx.x] = bidx;
-    __syncthreads();
-    for (int st = blockDim.x / 2; st > 0; st >>= 1) {
-      if (threadIdx.x < st) {
-        const int o = threadIdx.x + st;
-        if (bv_s[o] > bv_s[threadIdx.x] ||
-            (bv_s[o] == bv_s[threadIdx.x] && bi_s[o] < bi_s[threadIdx.x])) {
-          bv_s[threadIdx.x] = bv_s[o];
-          bf_s[threadIdx.x] = bf_s[o];
-          bi_s[threadIdx.x] = bi_s[o];
+    F[e] = f;
+  }
+  __syncthreads();
+  // canonical sign: one warp per column, argmax |F| with first-index ties
+  {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int k = warp; k < r; k += nw) {
+      double best = -1.0, bval = 0.0;
+      int64_t bidx = INT64_MAX;
+      for (int64_t i = lane; i < m; i += 32) {
+        const double f = F[i + m * k];
+        if (fabs(f) > best) {
+          best = fabs(f);
+          bval = f;
+          bidx = i;
         }
       }
-      __syncthreads();
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const double ov = __shfl_xor_sync(0xffffffffu, bval, o);
+        const int64_t oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+        if (ob > best || (ob == best && oi < bidx)) {
+          best = ob;
+          bval = ov;
+          bidx = oi;
+        }
+      }
+      if (lane == 0) sgn[k] = bval < 0.0 ? -1.0 : 1.0;
     }
-    if (threadIdx.x == 0) sgn[k] = bf_s[0] < 0.0 ? -1.0 : 1.0;
-    __syncthreads();
   }
+  __syncthreads();
   for (int64_t e = threadIdx.x; e < m * r; e += blockDim.x) {
     const double f = F[e] * sgn[e / m];
     F[e] = f;

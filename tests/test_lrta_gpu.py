@@ -47,6 +47,12 @@ CASES = [
     ((50, 60, 5), (16, 12), (4, 4), (3, 2), 0, "capped-lq", 0.3),
     ((30, 28, 9), (7, 6), (2, 2), (3, 3), 0, "log", 0.2),
     ((20, 22, 6), (5, 5), (2, 2), (2, 2), 0, "firm", 0.4),
+    # m % 32 == 0 in both modes: fused TMA panel passes + tcgen05 projection
+    ((128, 96, 10), (12, 10), (4, 4), (2, 2), 0, "mcp", 0.3),
+    # target rank = true rank: ranks above it would pick Ritz vectors in the
+    # pure-noise subspace, which are ill-conditioned for any implementation
+    ((256, 128, 8), (10, 10), (4, 4), (3, 3), 10, "l1", 0.2),
+    ((192, 160, 3, 4), (20, 18), (5, 6), (3, 2), 0, "scad", 0.25),
 ]
 
 
