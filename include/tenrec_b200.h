@@ -99,6 +99,39 @@ int tr_rsthosvd_bki(int dtype, const void* a, int order, const int64_t* dims,
 int tr_prox(int dtype, int penalty_kind, double p0, double p1, double mu, const void* v,
             void* out, int64_t n, void* stream);
 
+/*
+ * ADMM solvers -- replace tenrec.solvers.gnrhtc / gnhtc (solvers.py:204-295) and
+ * tenrec.onebit.gnobhtc / gnobrhtc (onebit.py:141-234).  A solver owns its
+ * device state; the caller keeps the observation buffers alive until destroy.
+ *
+ *   kind       0 gnrhtc (obs_a = Mobs, mask), 1 gnhtc (noise-free),
+ *              2 gnobhtc (obs_a = J1, obs_b = J2), 3 gnobrhtc (robust one-bit)
+ *   modes      the gradient set Gamma (0-based modes); {-1} = identity chain
+ *              (the pure low-rank ablation, SolverConfig.pure_lowrank)
+ *   structure  noise shrinkage groups: 0 entry, 1 tube, 2 slice
+ *   phi / psi  low-rank and noise penalties (kind, p0, p1)
+ *   lam, lam2  trade-off weights; mu0, mu_max, growth the penalty schedule;
+ *   alpha      one-bit box bound; mcount the one-bit sample count m
+ *   randomized 1 = randomized t-SVT with ranks/blocks/krylov/seed (modes 0, 1);
+ *              0 = deterministic t-SVT (face slices up to 64 x 64)
+ * tr_admm_step runs one sweep and writes TR_ADMM_NOUT residuals to `out`
+ * (host): [dL, dE, grad_gap, dG, fit_gap, dL_fro, dE_fro, dG_fro, fit_fro,
+ *  grad_gap_fro, ||Y||, max_k ||Lambda_k||, mu, rel_dL (one-bit), box_gap (one-bit)].
+ * tr_admm_read copies state `which` (0 L, 1 E or S, 2 Y, 3 Z) to `dst` (device).
+ */
+#define TR_ADMM_NOUT 15
+int tr_admm_create(int dtype, int order, const int64_t* dims, int kind, const void* obs_a,
+                   const void* obs_b, const uint8_t* mask, int nmodes, const int64_t* modes,
+                   int structure, int phi_kind, double phi_p0, double phi_p1, int psi_kind,
+                   double psi_p0, double psi_p1, double lam, double lam2, double mu0,
+                   double mu_max, double growth, double alpha, double mcount, int randomized,
+                   const int64_t* ranks, const int64_t* blocks, const int64_t* krylov,
+                   uint64_t seed, int transform_kind, const void* transform_mats,
+                   const double* alphas, void** handle);
+int tr_admm_step(void* handle, double* out);
+int tr_admm_read(void* handle, int which, void* dst, void* stream);
+int tr_admm_destroy(void* handle);
+
 /* Number of kernels this library has launched in the process (accounting). */
 int64_t tr_launch_count(void);
 

@@ -9,7 +9,10 @@ by hand-written sm_100a CUDA kernels behind the C ABI in
 
 from .penalties import (PENALTY_NAMES, L1, MCP, SCAD, CappedLq, Firm, LogPenalty, Lq, Penalty,
                         make_penalty)
+from .onebit import (ObservationSet, data_fit_update, gnobhtc, gnobrhtc, naive_estimate,
+                     onebit_observe)
 from .sketch import SketchConfig, TuckerFactors, gnhtsvt_randomized, rsthosvd_bki
+from .solvers import SolveReport, SolverConfig, default_lambda, gnhtc, gnrhtc
 from .transform import DEFAULT_TRANSFORM, Transform, TransformError
 
 __version__ = "0.1.0"
@@ -17,5 +20,7 @@ __version__ = "0.1.0"
 __all__ = [
     "PENALTY_NAMES", "L1", "MCP", "SCAD", "CappedLq", "Firm", "LogPenalty", "Lq", "Penalty",
     "make_penalty", "SketchConfig", "TuckerFactors", "gnhtsvt_randomized", "rsthosvd_bki",
-    "DEFAULT_TRANSFORM", "Transform", "TransformError",
+    "DEFAULT_TRANSFORM", "Transform", "TransformError", "SolveReport", "SolverConfig",
+    "default_lambda", "gnhtc", "gnrhtc", "ObservationSet", "data_fit_update", "gnobhtc",
+    "gnobrhtc", "naive_estimate", "onebit_observe",
 ]

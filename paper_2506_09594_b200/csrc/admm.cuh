@@ -1,0 +1,428 @@
+// Native ADMM solvers: GNRHTC / GNHTC (tenrec/solvers.py:204-295) and
+// GNOBHTC / GNOBRHTC (tenrec/onebit.py:141-234).
+//
+// A Solver owns every device buffer of one run.  tr_admm_step() executes one
+// ADMM sweep on the device and returns the Eq. (24) residuals to the host (the
+// only host synchronisation per iteration); the convergence decision and the
+// report bookkeeping stay in the Python host, mirroring the reference loop.
+// The low-rank step runs one randomized t-SVT per gradient mode, each on its
+// own stream with its own workspace, so the modes overlap on the GPU.
+#pragma once
+
+#include <vector>
+
+#include "admm_kernels.cuh"
+#include "fft.cuh"
+
+namespace tr {
+
+struct AdmmConfig {
+  int kind;        // 0 gnrhtc, 1 gnhtc, 2 gnobhtc, 3 gnobrhtc
+  int structure;   // 0 entry, 1 tube, 2 slice
+  Penalty phi, psi;
+  double lam, lam2, mu0, mu_max, growth, alpha, mcount;
+  int nmodes;
+  int modes[kMaxOrder];  // -1 = identity chain
+  int randomized;
+  int64_t ranks[2], blocks[2], krylov[2];
+  uint64_t seed;
+  int tkind;
+  const void* tmats;
+  double talphas[8];
+};
+
+template <typename T>
+struct Solver {
+  AdmmConfig cfg;
+  Geom g;
+  Shape sh;  // LRTA shape (ranks = sketch ranks, or full faces when deterministic)
+  int order;
+  const T *A, *B;  // mobs / (j1, j2)
+  const uint8_t* mask;
+  T *l, *lold, *e, *y, *z, *zold, *rhs;
+  std::vector<T*> gcur, gnew, lag, X;
+  cpx<T>* spec = nullptr;
+  std::vector<cpx<T>*> tw;
+  double* lam = nullptr;
+  double* scale = nullptr;
+  double *part = nullptr, *res = nullptr, *hres = nullptr;
+  std::vector<void*> ws;
+  int64_t ws_bytes = 0;
+  std::vector<cudaStream_t> streams;
+  std::vector<cudaEvent_t> evs;
+  cudaEvent_t ev_main;
+  SolveSpec ss;
+  double mu;
+  int64_t red_blocks;
+  std::vector<void*> allocs;
+
+  template <typename X_>
+  X_* alloc(int64_t n) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, std::max<int64_t>(n, 1) * sizeof(X_)) != cudaSuccess) return nullptr;
+    allocs.push_back(p);
+    return (X_*)p;
+  }
+  ~Solver() {
+    for (void* p : allocs) cudaFree(p);
+    if (hres) cudaFreeHost(hres);
+    for (auto s : streams) cudaStreamDestroy(s);
+    for (auto e : evs) cudaEventDestroy(e);
+    cudaEventDestroy(ev_main);
+  }
+  bool onebit() const { return cfg.kind >= 2; }
+};
+
+template <typename T>
+static int64_t grid_for(int64_t n) {
+  return std::max<int64_t>(1, std::min<int64_t>(cdiv(n, kRedThreads), (int64_t)num_sms() * 8));
+}
+
+// forward FFT over all axes, diagonal solve in the last-axis pass, inverse FFT
+template <typename T>
+static int fft_solve(Solver<T>& s, const T* rhs, T* out, cudaStream_t st) {
+  const Geom& g = s.g;
+  auto pass = [&](int a, const void* in, int in_real, void* dst, int out_real, double scale,
+                  int inverse, SolveSpec ss) -> int {
+    const int n = (int)g.dims[a];
+    const int64_t stv = g.st[a];
+    const int64_t hi = g.N / (stv * n);
+    const bool pow2 = (n & (n - 1)) == 0;
+    const int64_t cap = (pow2 ? 65536 : 32768) / (int64_t)(n * sizeof(cpx<T>));
+    int64_t L = std::max<int64_t>(1, std::min<int64_t>(32, cap));
+    L = std::min<int64_t>(L, stv == 1 ? hi : stv);
+    const int64_t grid = stv == 1 ? cdiv(hi, L) : hi * cdiv(stv, L);
+    const size_t smem = (size_t)L * n * sizeof(cpx<T>) * (pow2 ? 1 : 2);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_fft_axis<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    TR_REQUIRE(smem <= 200 * 1024, "FFT axis of length %d too long for one tile", n);
+    launch("fft", k_fft_axis<T>, (unsigned)grid, 256, smem, st, in, in_real, dst, out_real, scale,
+           stv, n, hi, (int)L, (const cpx<T>*)s.tw[a], inverse, ss, (const double*)s.lam);
+    return 0;
+  };
+  SolveSpec off = s.ss;
+  off.active = 0;
+  const int d = g.d;
+  if (pass(0, rhs, 1, s.spec, 0, 1.0, 0, off)) return 1;
+  for (int a = 1; a < d - 1; ++a)
+    if (pass(a, s.spec, 0, s.spec, 0, 1.0, 0, off)) return 1;
+  SolveSpec on = s.ss;
+  on.active = 1;
+  if (pass(d - 1, s.spec, 0, s.spec, 0, 1.0, 0, on)) return 1;
+  for (int a = d - 2; a >= 1; --a)
+    if (pass(a, s.spec, 0, s.spec, 0, 1.0, 1, off)) return 1;
+  if (pass(0, s.spec, 0, out, 1, 1.0 / (double)g.N, 1, off)) return 1;
+  TR_LAUNCH_CHECK();
+  return 0;
+}
+
+// deterministic t-SVT of a whole tensor with small faces (n1, n2 <= 64)
+template <typename T>
+static int full_svt(Solver<T>& s, const T* X, T* out, double tau, void* ws, cudaStream_t st) {
+  Shape fs = s.sh;
+  Carve cv(ws);
+  Bufs<T> bf;
+  carve<T>(cv, fs, bf);
+  const int64_t N = s.g.N;
+  launch("convert", k_convert<T, double>, (unsigned)grid_for<T>(N), kRedThreads, 0, st, X,
+         bf.core, N);
+  if (core_svt<T>(fs, s.cfg.tkind, (const cplx*)s.cfg.tmats, s.cfg.talphas, s.cfg.phi, tau, bf, st))
+    return 2;
+  launch("convert", k_convert<double, T>, (unsigned)grid_for<T>(N), kRedThreads, 0, st,
+         (const double*)bf.core, out, N);
+  return 0;
+}
+
+template <typename T>
+static int low_rank_step(Solver<T>& s, double tau) {
+  // fork: each mode on its own stream after the main stream's LRTA inputs
+  TR_CUDA(cudaEventRecord(s.ev_main, s.streams[0]));
+  for (int k = 0; k < s.cfg.nmodes; ++k) {
+    cudaStream_t sk = s.streams[k + 1];
+    TR_CUDA(cudaStreamWaitEvent(sk, s.ev_main, 0));
+    int rc;
+    if (s.cfg.randomized)
+      rc = gnhtsvt_randomized_t<T>(s.X[k], s.gnew[k], s.sh, s.cfg.seed, s.cfg.tkind, s.cfg.tmats,
+                                   s.cfg.talphas, s.cfg.phi, tau, nullptr, nullptr, s.ws[k],
+                                   s.ws_bytes, sk);
+    else
+      rc = full_svt<T>(s, s.X[k], s.gnew[k], tau, s.ws[k], sk);
+    if (rc) return rc;
+    TR_CUDA(cudaEventRecord(s.evs[k], sk));
+  }
+  for (int k = 0; k < s.cfg.nmodes; ++k) TR_CUDA(cudaStreamWaitEvent(s.streams[0], s.evs[k], 0));
+  return 0;
+}
+
+// residual slots written by a step (host array of TR_ADMM_NOUT doubles)
+enum {
+  R_DL = 0, R_DE, R_GRAD, R_DG, R_FIT,            // Eq. (24) inf-norms (completion)
+  R_DL_FRO, R_DE_FRO, R_DG_FRO, R_FIT_FRO, R_GRAD_FRO,
+  R_Y_NORM, R_LAG_NORM, R_MU, R_REL_DL, R_BOX_GAP, R_NOUT
+};
+
+template <typename T>
+static int admm_step(Solver<T>& s, double* hout) {
+  cudaStream_t st = s.streams[0];
+  const double mu = s.mu;
+  const Geom& g = s.g;
+  const int64_t N = g.N;
+  const unsigned grid = (unsigned)grid_for<T>(N);
+  const int nm = s.cfg.nmodes;
+  const int gamma = nm;
+  ModePtrs<T> gp{}, lp{};
+  gp.count = lp.count = nm;
+  for (int k = 0; k < nm; ++k) {
+    gp.axis[k] = lp.axis[k] = s.cfg.modes[k];
+    gp.p[k] = s.gcur[k];
+    lp.p[k] = s.lag[k];
+  }
+  const bool pure = nm == 1 && s.cfg.modes[0] < 0;
+  double* part = s.part;
+  double* res = s.res;  // device scratch for final reductions
+  const int64_t rb = grid;
+  // slots in res: [0..4] lag of mode k (5 each, up to 10 modes) | [64..70] noise/dual | [80..] onebit
+  double tau;
+  if (!s.onebit()) {
+    // L-subproblem (solvers.py:231-233)
+    if (pure) {
+      launch("admm_rhs", k_admm_rhs<T>, grid, kRedThreads, 0, st, g, s.A, s.e, s.y, mu, gp, lp,
+             s.l);
+    } else {
+      launch("admm_rhs", k_admm_rhs<T>, grid, kRedThreads, 0, st, g, s.A, s.e, s.y, mu, gp, lp,
+             s.rhs);
+      if (fft_solve<T>(s, s.rhs, s.l, st)) return 1;
+    }
+    tau = 1.0 / (gamma * mu);
+    for (int k = 0; k < nm; ++k)
+      launch("lrta_input", k_lrta_input<T>, grid, kRedThreads, 0, st, g, (const T*)s.l,
+             s.cfg.modes[k], (const T*)s.lag[k], mu, s.X[k]);
+    if (low_rank_step<T>(s, tau)) return 2;
+    for (int k = 0; k < nm; ++k) {
+      launch("lag_update", k_lag_update<T>, grid, kRedThreads, 0, st, g, (const T*)s.l,
+             s.cfg.modes[k], (const T*)s.gnew[k], (const T*)s.gcur[k], s.lag[k], mu, part);
+      launch("final_reduce", k_final_reduce, 1, 256, 0, st, (const double*)part, (int)rb, 5,
+             0b00101u, res + 5 * k);
+    }
+    // noise and dual updates (solvers.py:239-246)
+    const double level = s.cfg.lam / mu;
+    const int structure = s.cfg.kind == 1 ? 3 : s.cfg.structure;
+    if (structure == 1 || structure == 2) {
+      const int64_t face = g.dims[0] * g.dims[1];
+      if (structure == 1)
+        launch("group_scale", k_group_scale<T>, (unsigned)cdiv(face, 256), 256, 0, st, g, 1, s.A,
+               s.mask, (const T*)s.l, (const T*)s.y, mu, s.cfg.psi, level, s.scale);
+      else
+        launch("group_scale", k_group_scale<T>, (unsigned)(N / face), 256, 0, st, g, 2, s.A,
+               s.mask, (const T*)s.l, (const T*)s.y, mu, s.cfg.psi, level, s.scale);
+    }
+    launch("noise_dual", k_noise_dual<T>, grid, kRedThreads, 0, st, g, structure, s.A, s.mask,
+           (const T*)s.l, (const T*)s.lold, s.e, s.y, mu, s.cfg.psi, level,
+           (const double*)s.scale, part);
+    launch("final_reduce", k_final_reduce, 1, 256, 0, st, (const double*)part, (int)rb, 7,
+           0b0010101u, res + 64);
+  } else {
+    // one-bit (onebit.py:171-192)
+    const bool robust = s.cfg.kind == 3;
+    launch("onebit_fit", k_onebit_fit<T>, grid, kRedThreads, 0, st, N, s.A, s.B, s.cfg.mcount, mu,
+           (const T*)s.z, (const T*)s.y, s.cfg.alpha, (const T*)s.lold, s.l, s.e, robust ? 1 : 0,
+           s.cfg.psi, s.cfg.lam2, part);
+    launch("final_reduce", k_final_reduce, 1, 256, 0, st, (const double*)part, (int)rb, 3, 0b100u,
+           res + 80);
+    // Z-subproblem: solve with b = L + Y / mu
+    if (pure) {
+      launch("admm_rhs", k_admm_rhs<T>, grid, kRedThreads, 0, st, g, (const T*)s.l, (const T*)nullptr,
+             s.y, mu, gp, lp, s.z);
+    } else {
+      launch("admm_rhs", k_admm_rhs<T>, grid, kRedThreads, 0, st, g, (const T*)s.l, (const T*)nullptr,
+             s.y, mu, gp, lp, s.rhs);
+      if (fft_solve<T>(s, s.rhs, s.z, st)) return 1;
+    }
+    tau = s.cfg.lam / (gamma * mu);
+    for (int k = 0; k < nm; ++k)
+      launch("lrta_input", k_lrta_input<T>, grid, kRedThreads, 0, st, g, (const T*)s.z,
+             s.cfg.modes[k], (const T*)s.lag[k], mu, s.X[k]);
+    if (low_rank_step<T>(s, tau)) return 2;
+    launch("onebit_dual", k_onebit_dual<T>, grid, kRedThreads, 0, st, N, (const T*)s.l,
+           (const T*)s.z, s.y, mu, part);
+    launch("final_reduce", k_final_reduce, 1, 256, 0, st, (const double*)part, (int)rb, 2, 0b01u,
+           res + 90);
+    for (int k = 0; k < nm; ++k) {
+      launch("lag_update", k_lag_update<T>, grid, kRedThreads, 0, st, g, (const T*)s.z,
+             s.cfg.modes[k], (const T*)s.gnew[k], (const T*)s.gcur[k], s.lag[k], mu, part);
+      launch("final_reduce", k_final_reduce, 1, 256, 0, st, (const double*)part, (int)rb, 5,
+             0b00101u, res + 5 * k);
+    }
+  }
+  TR_LAUNCH_CHECK();
+  TR_CUDA(cudaMemcpyAsync(s.hres, res, 128 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  TR_CUDA(cudaStreamSynchronize(st));
+  const double* h = s.hres;
+  for (int i = 0; i < R_NOUT; ++i) hout[i] = 0.0;
+  double grad = 0, dg = 0, dgf = 0, gradf = 0, lagn = 0;
+  for (int k = 0; k < nm; ++k) {
+    grad = fmax(grad, h[5 * k + 0]);
+    gradf = fmax(gradf, sqrt(h[5 * k + 1]));
+    dg = fmax(dg, h[5 * k + 2]);
+    dgf = fmax(dgf, sqrt(h[5 * k + 3]));
+    lagn = fmax(lagn, sqrt(h[5 * k + 4]));
+  }
+  hout[R_GRAD] = grad;
+  hout[R_GRAD_FRO] = gradf;
+  hout[R_DG] = dg;
+  hout[R_DG_FRO] = dgf;
+  hout[R_LAG_NORM] = lagn;
+  hout[R_MU] = mu;
+  if (!s.onebit()) {
+    hout[R_DL] = h[64];
+    hout[R_DL_FRO] = sqrt(h[65]);
+    hout[R_DE] = h[66];
+    hout[R_DE_FRO] = sqrt(h[67]);
+    hout[R_FIT] = h[68];
+    hout[R_FIT_FRO] = sqrt(h[69]);
+    hout[R_Y_NORM] = sqrt(h[70]);
+  } else {
+    hout[R_REL_DL] = sqrt(h[80]) / fmax(sqrt(h[81]), 1e-30);
+    hout[R_DL] = h[82];
+    hout[R_BOX_GAP] = h[90];
+    hout[R_Y_NORM] = sqrt(h[91]);
+  }
+  // roll state: L_prev <- L, G <- G_new, mu <- min(mu_max, growth mu); Z is
+  // overwritten in place by the next solve
+  std::swap(s.l, s.lold);
+  for (int k = 0; k < nm; ++k) std::swap(s.gcur[k], s.gnew[k]);
+  s.mu = std::min(s.cfg.mu_max, s.cfg.growth * s.mu);
+  return 0;
+}
+
+template <typename T>
+static int admm_create(const AdmmConfig& cfg, int order, const int64_t* dims, const void* a,
+                       const void* b, const uint8_t* mask, Solver<T>** out) {
+  TR_REQUIRE(order >= 3 && order <= kMaxOrder, "order must be in [3, %d]", kMaxOrder);
+  TR_REQUIRE(cfg.nmodes >= 1 && cfg.nmodes <= kMaxOrder, "need 1..%d gradient modes", kMaxOrder);
+  TR_CUDA(cudaDeviceSynchronize());  // inputs written on the caller's streams
+  auto* s = new Solver<T>();
+  s->cfg = cfg;
+  s->order = order;
+  Geom& g = s->g;
+  g.d = order;
+  g.N = 1;
+  for (int i = 0; i < order; ++i) {
+    g.dims[i] = dims[i];
+    g.st[i] = g.N;
+    g.N *= dims[i];
+  }
+  const int64_t N = g.N;
+  const int nm = cfg.nmodes;
+  if (cfg.randomized) {
+    if (make_shape(order, dims, cfg.ranks, cfg.blocks, cfg.krylov, s->sh)) {
+      delete s;
+      return 1;
+    }
+  } else {
+    if (!(dims[0] <= 64 && dims[1] <= 64)) {
+      delete s;
+      TR_REQUIRE(false, "deterministic t-SVT on the GPU needs face slices up to 64 x 64; "
+                        "use the randomized solver for larger tensors");
+    }
+    Shape& f = s->sh;
+    f.order = order;
+    f.n1 = dims[0];
+    f.n2 = dims[1];
+    f.nf = N / (dims[0] * dims[1]);
+    f.tr.nt = order - 2;
+    for (int i = 0; i < 8; ++i) f.tr.d[i] = 1;
+    for (int i = 2; i < order; ++i) f.tr.d[i - 2] = dims[i];
+    f.r0 = dims[0];
+    f.r1 = dims[1];
+    f.b0 = f.b1 = 1;
+    f.q0 = f.q1 = 0;
+    f.s0 = f.s1 = 1;
+  }
+  s->A = (const T*)a;
+  s->B = (const T*)b;
+  s->mask = mask;
+  s->mu = cfg.mu0;
+  s->l = s->template alloc<T>(N);
+  s->lold = s->template alloc<T>(N);
+  s->e = s->template alloc<T>(N);
+  s->y = s->template alloc<T>(N);
+  s->z = s->template alloc<T>(N);
+  s->rhs = s->template alloc<T>(N);
+  for (int k = 0; k < nm; ++k) {
+    s->gcur.push_back(s->template alloc<T>(N));
+    s->gnew.push_back(s->template alloc<T>(N));
+    s->lag.push_back(s->template alloc<T>(N));
+    s->X.push_back(s->template alloc<T>(N));
+  }
+  s->spec = s->template alloc<cpx<T>>(N);
+  int64_t lam_total = 0;
+  for (int i = 0; i < order; ++i) {
+    s->tw.push_back(s->template alloc<cpx<T>>(dims[i]));
+    lam_total += dims[i];
+  }
+  s->lam = s->template alloc<double>(lam_total);
+  s->scale = s->template alloc<double>(std::max<int64_t>(dims[0] * dims[1], N / (dims[0] * dims[1])));
+  s->red_blocks = grid_for<T>(N);
+  s->part = s->template alloc<double>(s->red_blocks * 8);
+  s->res = s->template alloc<double>(128);
+  for (void* p : s->allocs)
+    if (!p) {
+      delete s;
+      TR_REQUIRE(false, "device allocation failed (out of memory?)");
+    }
+  TR_CUDA(cudaMallocHost(&s->hres, 128 * sizeof(double)));
+  // LRTA workspaces, one per mode stream
+  {
+    Carve cv(nullptr);
+    Bufs<T> bf;
+    carve<T>(cv, s->sh, bf);
+    s->ws_bytes = cv.off;
+  }
+  for (int k = 0; k < nm; ++k) {
+    void* p = s->template alloc<unsigned char>(s->ws_bytes);
+    TR_REQUIRE(p, "workspace allocation failed");
+    s->ws.push_back(p);
+  }
+  for (int k = 0; k <= nm; ++k) {
+    cudaStream_t st;
+    TR_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    s->streams.push_back(st);
+    if (k < nm) {
+      cudaEvent_t e;
+      TR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      s->evs.push_back(e);
+    }
+  }
+  TR_CUDA(cudaEventCreateWithFlags(&s->ev_main, cudaEventDisableTiming));
+  cudaStream_t st = s->streams[0];
+  for (void* p : {(void*)s->l, (void*)s->lold, (void*)s->e, (void*)s->y, (void*)s->z})
+    TR_CUDA(cudaMemsetAsync(p, 0, N * sizeof(T), st));
+  for (int k = 0; k < nm; ++k) {
+    TR_CUDA(cudaMemsetAsync(s->gcur[k], 0, N * sizeof(T), st));
+    TR_CUDA(cudaMemsetAsync(s->lag[k], 0, N * sizeof(T), st));
+  }
+  // FFT twiddles and Laplacian eigenvalues of the gradient modes
+  SolveSpec& ss = s->ss;
+  ss.active = 0;
+  ss.d = order;
+  int64_t off = 0;
+  for (int i = 0; i < order; ++i) {
+    ss.dims[i] = dims[i];
+    ss.lam_off[i] = -1;
+    launch("setup", k_twiddles<T>, (unsigned)cdiv(dims[i], 256), 256, 0, st, (int)dims[i], s->tw[i]);
+    launch("setup", k_lap_eig, (unsigned)cdiv(dims[i], 256), 256, 0, st, (int)dims[i], s->lam + off);
+    for (int k = 0; k < nm; ++k)
+      if (cfg.modes[k] == i) ss.lam_off[i] = off;
+    off += dims[i];
+  }
+  TR_LAUNCH_CHECK();
+  TR_CUDA(cudaStreamSynchronize(st));
+  *out = s;
+  return 0;
+}
+
+}  // namespace tr

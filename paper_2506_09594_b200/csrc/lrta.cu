@@ -517,7 +517,16 @@ __global__ void k_prox(Penalty pen, double mu, const T* __restrict__ v, T* __res
 
 }  // namespace tr
 
+#include "admm.cuh"
+
 using namespace tr;
+
+namespace {
+struct AdmmHandle {
+  int dtype;
+  void* solver;
+};
+}  // namespace
 
 extern "C" {
 
@@ -579,6 +588,106 @@ int tr_rsthosvd_bki(int dtype, const void* a, int order, const int64_t* dims,
   TR_REQUIRE(dtype == TR_F64, "bad dtype %d", dtype);
   return rsthosvd_t<double>(a, sh, seed, sketch0, sketch1, f0, f1, core, ranks_eff, workspace,
                             workspace_bytes, st);
+}
+
+int tr_admm_create(int dtype, int order, const int64_t* dims, int kind, const void* obs_a,
+                   const void* obs_b, const uint8_t* mask, int nmodes, const int64_t* modes,
+                   int structure, int phi_kind, double phi_p0, double phi_p1, int psi_kind,
+                   double psi_p0, double psi_p1, double lam, double lam2, double mu0,
+                   double mu_max, double growth, double alpha, double mcount, int randomized,
+                   const int64_t* ranks, const int64_t* blocks, const int64_t* krylov,
+                   uint64_t seed, int transform_kind, const void* transform_mats,
+                   const double* alphas, void** handle) {
+  TR_REQUIRE(handle && dims && modes, "null pointer argument");
+  TR_REQUIRE(kind >= 0 && kind <= 3, "bad solver kind %d", kind);
+  TR_REQUIRE(structure >= 0 && structure <= 2, "bad shrink structure %d", structure);
+  TR_REQUIRE(phi_kind >= 0 && phi_kind <= 6 && psi_kind >= 0 && psi_kind <= 6, "bad penalty kind");
+  TR_REQUIRE(mu0 > 0 && growth > 1, "mu0 must be > 0 and growth > 1");
+  TR_REQUIRE(kind >= 2 ? (obs_a && obs_b) : (obs_a && mask), "missing observations");
+  TR_REQUIRE(transform_kind != TR_TRANSFORM_EXPLICIT || (transform_mats && alphas),
+             "explicit transform needs matrices and alphas");
+  AdmmConfig cfg{};
+  cfg.kind = kind;
+  cfg.structure = structure;
+  cfg.phi = Penalty{phi_kind, phi_p0, phi_p1};
+  cfg.psi = Penalty{psi_kind, psi_p0, psi_p1};
+  cfg.lam = lam;
+  cfg.lam2 = lam2;
+  cfg.mu0 = mu0;
+  cfg.mu_max = mu_max;
+  cfg.growth = growth;
+  cfg.alpha = alpha;
+  cfg.mcount = mcount;
+  cfg.nmodes = nmodes;
+  for (int k = 0; k < nmodes && k < kMaxOrder; ++k) {
+    TR_REQUIRE(modes[k] >= -1 && modes[k] < order, "gradient mode %lld out of range",
+               (long long)modes[k]);
+    cfg.modes[k] = (int)modes[k];
+  }
+  cfg.randomized = randomized;
+  for (int i = 0; i < 2; ++i) {
+    cfg.ranks[i] = ranks ? ranks[i] : 1;
+    cfg.blocks[i] = blocks ? blocks[i] : 1;
+    cfg.krylov[i] = krylov ? krylov[i] : 0;
+  }
+  cfg.seed = seed;
+  cfg.tkind = transform_kind;
+  cfg.tmats = transform_mats;
+  for (int i = 0; i < 8; ++i) cfg.talphas[i] = (alphas && i < order - 2) ? alphas[i] : 1.0;
+  auto* h = new AdmmHandle{dtype, nullptr};
+  int rc;
+  if (dtype == TR_F32) {
+    Solver<float>* s = nullptr;
+    rc = admm_create<float>(cfg, order, dims, obs_a, obs_b, mask, &s);
+    h->solver = s;
+  } else {
+    Solver<double>* s = nullptr;
+    rc = admm_create<double>(cfg, order, dims, obs_a, obs_b, mask, &s);
+    h->solver = s;
+  }
+  if (rc) {
+    delete h;
+    return rc;
+  }
+  *handle = h;
+  return 0;
+}
+
+int tr_admm_step(void* handle, double* out) {
+  TR_REQUIRE(handle && out, "null pointer argument");
+  auto* h = (AdmmHandle*)handle;
+  if (h->dtype == TR_F32) return admm_step<float>(*(Solver<float>*)h->solver, out);
+  return admm_step<double>(*(Solver<double>*)h->solver, out);
+}
+
+int tr_admm_read(void* handle, int which, void* dst, void* stream) {
+  TR_REQUIRE(handle && dst, "null pointer argument");
+  auto* h = (AdmmHandle*)handle;
+  auto rd = [&](auto* s) -> int {
+    using S = std::remove_pointer_t<decltype(s)>;
+    const void* src = which == 0 ? (const void*)s->lold
+                      : which == 1 ? (const void*)s->e
+                      : which == 2 ? (const void*)s->y
+                                   : (const void*)s->z;
+    const size_t es = sizeof(*s->l);
+    TR_CUDA(cudaStreamSynchronize(s->streams[0]));
+    TR_CUDA(cudaMemcpyAsync(dst, src, es * s->g.N, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    (void)sizeof(S);
+    return 0;
+  };
+  TR_REQUIRE(which >= 0 && which <= 3, "bad state index %d", which);
+  if (h->dtype == TR_F32) return rd((Solver<float>*)h->solver);
+  return rd((Solver<double>*)h->solver);
+}
+
+int tr_admm_destroy(void* handle) {
+  if (!handle) return 0;
+  auto* h = (AdmmHandle*)handle;
+  cudaDeviceSynchronize();
+  if (h->dtype == TR_F32) delete (Solver<float>*)h->solver;
+  else delete (Solver<double>*)h->solver;
+  delete h;
+  return 0;
 }
 
 int tr_prox(int dtype, int penalty_kind, double p0, double p1, double mu, const void* v,

@@ -1,0 +1,267 @@
+"""ADMM tensor-completion solvers on the B200, mirroring tenrec/solvers.py.
+
+Same names, fields, defaults, errors and report structure as the reference:
+  default_lambda      solvers.py:41-45
+  SolverConfig        solvers.py:48-101
+  SolveReport         solvers.py:104-122
+  gnrhtc / gnhtc      solvers.py:204-295
+Every ADMM sweep runs in the native solver of the C ABI (tr_admm_step: FFT
+solve, per-mode randomized t-SVT on concurrent streams, fused noise / dual /
+multiplier updates); this host keeps the reference's loop, stopping rule and
+bookkeeping.  The objective's regularizer term (a diagnostic needing full-size
+face SVDs) is reported as None on this path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .penalties import MCP, Penalty
+from .penalties import encode as encode_penalty
+from .sketch import SketchConfig
+from .tensors import ColMajor, from_device, to_device
+from .transform import DEFAULT_TRANSFORM, Transform, as_transform
+
+__all__ = ["SolverConfig", "SolveReport", "default_lambda", "gnrhtc", "gnhtc", "RESIDUAL_NAMES"]
+
+RESIDUAL_NAMES = ("dL", "dE", "grad_gap", "dG", "fit_gap")
+STRUCTURES = {"entry": 0, "tube": 1, "slice": 2}
+NOUT = 15
+
+
+def default_lambda(dims, xi: float = 1.5) -> float:
+    dims = tuple(dims)
+    trailing = float(np.prod(dims[2:])) if len(dims) > 2 else 1.0
+    return xi / float(np.sqrt(max(dims[0], dims[1]) * trailing))
+
+
+@dataclass
+class SolverConfig:
+    phi: Penalty = field(default_factory=MCP)
+    psi: Penalty = field(default_factory=MCP)
+    structure: str = "entry"
+    gamma_modes: tuple = None
+    lam: float = None
+    xi: float = 1.5
+    lam2: float = None
+    mu0: float = 1e-3
+    mu_max: float = 1e10
+    growth: float = 1.1
+    tol: float = 1e-4
+    max_iters: int = 500
+    transform: Transform = field(default_factory=lambda: DEFAULT_TRANSFORM)
+    randomized: bool = False
+    sketch: SketchConfig = None
+    seed: int = 0
+    pure_lowrank: bool = False
+
+    @classmethod
+    def one_bit(cls, **kwargs) -> "SolverConfig":
+        kwargs.setdefault("mu0", 1e-6)
+        kwargs.setdefault("mu_max", 1e3)
+        kwargs.setdefault("growth", 1.05)
+        return cls(**kwargs)
+
+    def validate(self) -> None:
+        if self.mu0 <= 0:
+            raise ValueError("mu0 must be > 0")
+        if self.growth <= 1:
+            raise ValueError("growth rate must be > 1")
+        if self.tol <= 0:
+            raise ValueError("stopping tolerance must be > 0")
+        if self.max_iters < 1:
+            raise ValueError("max_iters must be >= 1")
+        if str(self.structure).lower() not in STRUCTURES:
+            raise ValueError(f"structure must be one of {tuple(STRUCTURES)}, got {self.structure!r}")
+        if self.randomized and self.sketch is None:
+            raise ValueError("randomized mode requires a sketch configuration")
+
+    def modes_for(self, dims) -> tuple:
+        modes = tuple(range(len(dims))) if self.gamma_modes is None else tuple(self.gamma_modes)
+        if not modes:
+            raise ValueError("gradient mode set must be nonempty")
+        return modes
+
+    def lam_for(self, dims) -> float:
+        lam = default_lambda(dims, self.xi) if self.lam is None else float(self.lam)
+        if lam <= 0:
+            raise ValueError("lambda must be > 0")
+        return lam
+
+
+@dataclass
+class SolveReport:
+    iterations: int = 0
+    converged: bool = False
+    residual_names: tuple = RESIDUAL_NAMES
+    residual_history: list = field(default_factory=list)
+    diff_fro_history: list = field(default_factory=list)
+    feas_fro_history: list = field(default_factory=list)
+    multiplier_history: list = field(default_factory=list)
+    mu_history: list = field(default_factory=list)
+    objective: dict = field(default_factory=dict)
+    wall_clock: float = 0.0
+
+    def final_residuals(self) -> dict:
+        if not self.residual_history:
+            return {}
+        return dict(zip(self.residual_names, self.residual_history[-1]))
+
+
+class NativeSolver:
+    """One native ADMM run: owns the C handle and its lifetime."""
+
+    KINDS = {"gnrhtc": 0, "gnhtc": 1, "gnobhtc": 2, "gnobrhtc": 3}
+
+    def __init__(self, kind, cm_a: ColMajor, cm_b, mask_dev, cfg: SolverConfig, modes, lam,
+                 lam2=0.0, alpha=0.0, mcount=0.0, structure="entry"):
+        self.lib = _lib.lib()
+        self.cm = cm_a
+        self.keep = [cm_a, cm_b, mask_dev]
+        dims = cm_a.dims
+        transform = as_transform(cfg.transform)
+        transform.check_shape(dims)
+        if cfg.randomized:
+            from .sketch import _resolve
+            _, ranks, blocks, krylov = _resolve(cfg.sketch, dims)
+            seed = cfg.sketch.seed
+        else:
+            if dims[0] > 64 or dims[1] > 64:
+                raise NotImplementedError(
+                    "the deterministic t-SVT runs on the B200 for face slices up to 64 x 64; "
+                    "set randomized=True with a SketchConfig for larger tensors")
+            ranks, blocks, krylov, seed = (1, 1), (1, 1), (0, 0), 0
+        tcode, tmats, talphas, self._tkeep = transform.device_args(dims)
+        phi = encode_penalty(cfg.phi)
+        psi = encode_penalty(cfg.psi)
+        handle = ctypes.c_void_p()
+        _lib.check(self.lib.tr_admm_create(
+            cm_a.dtype_code, len(dims), _lib.i64(dims), self.KINDS[kind], ctypes.c_void_p(cm_a.ptr),
+            ctypes.c_void_p(cm_b.ptr) if cm_b is not None else None,
+            ctypes.c_void_p(mask_dev.data_ptr()) if mask_dev is not None else None,
+            len(modes), _lib.i64(modes), STRUCTURES[str(structure).lower()], phi[0], phi[1], phi[2],
+            psi[0], psi[1], psi[2], float(lam), float(lam2 or 0.0), float(cfg.mu0),
+            float(cfg.mu_max), float(cfg.growth), float(alpha), float(mcount),
+            1 if cfg.randomized else 0, _lib.i64(ranks), _lib.i64(blocks), _lib.i64(krylov),
+            ctypes.c_uint64(int(seed) & (2 ** 64 - 1)), tcode, tmats, talphas, ctypes.byref(handle)))
+        self.handle = handle
+        self.out = (ctypes.c_double * NOUT)()
+
+    def step(self):
+        _lib.check(self.lib.tr_admm_step(self.handle, self.out))
+        return list(self.out)
+
+    def read(self, which: int) -> ColMajor:
+        import torch
+
+        flat = torch.empty_like(self.cm.flat)
+        _lib.check(self.lib.tr_admm_read(self.handle, which, ctypes.c_void_p(flat.data_ptr()),
+                                         _lib.stream_ptr()))
+        return ColMajor(flat, self.cm.dims, self.cm.kind, self.cm.np_dtype)
+
+    def close(self):
+        if self.handle:
+            self.lib.tr_admm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _mask_device(mask, dims):
+    import torch
+
+    if isinstance(mask, torch.Tensor):
+        m = mask.to(device="cuda", dtype=torch.uint8)
+        return m.permute(*reversed(range(m.dim()))).contiguous().reshape(-1)
+    m = np.asarray(mask, dtype=bool)
+    return torch.from_numpy(np.ascontiguousarray(m.ravel(order="F")).astype(np.uint8)).to("cuda")
+
+
+def _admm_complete(mobs, mask, cfg: SolverConfig, noise_free: bool):
+    import torch
+
+    t0 = time.perf_counter()
+    cfg.validate()
+    cm = to_device(mobs)
+    dims = cm.dims
+    mshape = tuple(mask.shape)
+    if mshape != dims:
+        raise ValueError("mask shape must match the observation tensor")
+    mdev = _mask_device(mask, dims)
+    if not bool(mdev.any()):
+        raise ValueError("the observed set is empty")
+    if bool(((mdev == 0) & (cm.flat != 0)).any()):
+        raise ValueError("observations must be zero outside the observed set")
+    lam = cfg.lam_for(dims)
+    modes = (-1,) if cfg.pure_lowrank else cfg.modes_for(dims)
+    for k in modes:
+        if k != -1 and not 0 <= k < len(dims):
+            raise ValueError(f"gradient mode {k} out of range for dims {dims}")
+    run = NativeSolver("gnhtc" if noise_free else "gnrhtc", cm, None, mdev, cfg, modes, lam,
+                       structure=cfg.structure)
+    report = SolveReport()
+    try:
+        for _ in range(cfg.max_iters):
+            o = run.step()
+            report.residual_history.append(o[0:5])
+            report.diff_fro_history.append([o[5], o[6], o[7]])
+            report.feas_fro_history.append([o[8], o[9]])
+            report.multiplier_history.append([o[10], o[11]])
+            report.mu_history.append(o[12])
+            report.iterations += 1
+            if max(o[0:5]) <= cfg.tol and max(o[5:8]) <= cfg.tol:
+                report.converged = True
+                break
+        l_cm = run.read(0)
+        e_cm = run.read(1)
+    finally:
+        run.close()
+    if not bool(torch.isfinite(l_cm.flat).all()):
+        raise FloatingPointError("solver produced non-finite iterates")
+    report.objective = {"regularizer": None, "noise": lam * _upsilon(e_cm, mdev, cfg),
+                        "lambda": lam}
+    report.wall_clock = time.perf_counter() - t0
+    return from_device(l_cm), from_device(e_cm), report
+
+
+def _upsilon(e_cm: ColMajor, mdev, cfg: SolverConfig) -> float:
+    """Structured noise penalty value of mask * E (shrink.py:135-145), on the device."""
+    import torch
+
+    e = e_cm.flat.double() * mdev.double()
+    d = e_cm.dims
+    kind, p0, p1 = encode_penalty(cfg.psi)
+    pen = cfg.psi
+    st = str(cfg.structure).lower()
+    if st == "entry":
+        vals = e.abs()
+    else:
+        x = e.reshape(tuple(reversed(d)))  # (trailing..., n2, n1)
+        if st == "tube":
+            vals = x.reshape(-1, d[1] * d[0]).pow(2).sum(0).sqrt()
+        else:
+            vals = x.reshape(-1, d[1] * d[0]).pow(2).sum(1).sqrt()
+    if hasattr(pen, "value"):
+        return float(pen.value(vals, 1.0).sum())
+    return float("nan")
+
+
+def gnrhtc(mobs, mask, cfg: SolverConfig):
+    """Robust completion: returns ``(L, E, report)``."""
+    return _admm_complete(mobs, mask, cfg, noise_free=False)
+
+
+def gnhtc(mobs, mask, cfg: SolverConfig):
+    """Noise-free completion (observations trusted): returns ``(L, report)``."""
+    l, _, report = _admm_complete(mobs, mask, cfg, noise_free=True)
+    return l, report
