@@ -131,6 +131,8 @@ int tr_admm_create(int dtype, int order, const int64_t* dims, int kind, const vo
 int tr_admm_step(void* handle, double* out);
 int tr_admm_read(void* handle, int which, void* dst, void* stream);
 int tr_admm_destroy(void* handle);
+/* The solver's main cudaStream_t (every sweep starts and ends on it). */
+void* tr_admm_stream(void* handle);
 
 /* Number of kernels this library has launched in the process (accounting). */
 int64_t tr_launch_count(void);

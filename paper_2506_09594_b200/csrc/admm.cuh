@@ -79,42 +79,100 @@ static int64_t grid_for(int64_t n) {
 }
 
 // forward FFT over all axes, diagonal solve in the last-axis pass, inverse FFT
+// Spectrum geometry: half spectrum along axis 0 (n0/2+1 bins) when n0 is even
+// (real-to-complex first pass), the full complex spectrum otherwise.
+struct SpecGeom {
+  bool half;
+  int64_t dims[kMaxOrder], st[kMaxOrder], N;
+};
+
+static SpecGeom spec_geom(const Geom& g) {
+  SpecGeom sg;
+  sg.half = g.dims[0] % 2 == 0 && g.dims[0] >= 2;
+  sg.N = 1;
+  for (int a = 0; a < g.d; ++a) {
+    sg.dims[a] = (a == 0 && sg.half) ? g.dims[0] / 2 + 1 : g.dims[a];
+    sg.st[a] = sg.N;
+    sg.N *= sg.dims[a];
+  }
+  return sg;
+}
+
+// forward FFT over all axes, diagonal solve in the last-axis pass, inverse FFT
 template <typename T>
 static int fft_solve(Solver<T>& s, const T* rhs, T* out, cudaStream_t st) {
   const Geom& g = s.g;
-  auto pass = [&](int a, const void* in, int in_real, void* dst, int out_real, double scale,
-                  int inverse, SolveSpec ss) -> int {
+  const SpecGeom sg = spec_geom(g);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_fft_axis<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  // mode: FFT_C2C on spectrum axis a, or FFT_R2C / FFT_C2R on axis 0
+  auto pass = [&](int a, int mode, const void* in, void* dst, double scale, int inverse,
+                  SolveSpec ss) -> int {
     const int n = (int)g.dims[a];
-    const int64_t stv = g.st[a];
-    const int64_t hi = g.N / (stv * n);
-    const bool pow2 = (n & (n - 1)) == 0;
-    const int64_t cap = (pow2 ? 65536 : 32768) / (int64_t)(n * sizeof(cpx<T>));
-    int64_t L = std::max<int64_t>(1, std::min<int64_t>(32, cap));
-    L = std::min<int64_t>(L, stv == 1 ? hi : stv);
-    const int64_t grid = stv == 1 ? cdiv(hi, L) : hi * cdiv(stv, L);
-    const size_t smem = (size_t)L * n * sizeof(cpx<T>) * (pow2 ? 1 : 2);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_fft_axis<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr = true;
+    const int nt = mode == FFT_C2C ? n : n / 2;
+    const int64_t stv = mode == FFT_C2C ? sg.st[a] : 1;
+    const int64_t hi = mode == FFT_C2C ? sg.N / (stv * n) : g.N / n;
+    const bool pow2 = (nt & (nt - 1)) == 0;
+    // persistent double-buffered kernel: pow2, <= 2048-point tiles, 16B-aligned real lines
+    const bool persistent = pow2 && nt >= 8 && nt <= 2048 &&
+                            (mode != FFT_R2C || (n * (int64_t)sizeof(T)) % 16 == 0) &&
+                            getenv("TR_FFT_SIMPLE") == nullptr;
+    if (persistent) {
+      static bool pattr = false;
+      if (!pattr) {
+        cudaFuncSetAttribute(k_fft_p2<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        pattr = true;
+      }
+      const int64_t cap = std::min<int64_t>(std::min<int64_t>(16, 2048 / nt), stv == 1 ? hi : stv);
+      int lL = 0;
+      while ((2ll << lL) <= cap) ++lL;  // largest power of two <= cap
+      const int64_t L = 1ll << lL;
+      const int64_t ntiles = stv == 1 ? cdiv(hi, L) : hi * cdiv(stv, L);
+      const int64_t grid = std::min<int64_t>(ntiles, 2 * (int64_t)num_sms());
+      const size_t smem = ((size_t)nt + 2 * (size_t)L * (nt + 1)) * sizeof(cpx<T>);
+      launch("fft", k_fft_p2<T>, (unsigned)grid, 256, smem, st, in, dst, mode, scale, stv, n, hi,
+             lL, ntiles, (const cpx<T>*)s.tw[a], inverse, ss, (const double*)s.lam);
+      return 0;
     }
+    // at most 4096 complex line elements per CTA (8 radix-2 groups per thread)
+    int64_t L = std::max<int64_t>(1, std::min<int64_t>(16, 4096 / nt));
+    L = std::min<int64_t>(L, stv == 1 ? hi : stv);
+    TR_REQUIRE(nt <= 4096, "FFT axis of length %d exceeds the 4096-point tile", n);
+    const int64_t grid = stv == 1 ? cdiv(hi, L) : hi * cdiv(stv, L);
+    const size_t smem = ((size_t)nt + (size_t)L * nt * (pow2 ? 1 : 2)) * sizeof(cpx<T>);
     TR_REQUIRE(smem <= 200 * 1024, "FFT axis of length %d too long for one tile", n);
-    launch("fft", k_fft_axis<T>, (unsigned)grid, 256, smem, st, in, in_real, dst, out_real, scale,
-           stv, n, hi, (int)L, (const cpx<T>*)s.tw[a], inverse, ss, (const double*)s.lam);
+    launch("fft", k_fft_axis<T>, (unsigned)grid, 256, smem, st, in, dst, mode, scale, stv, n, hi,
+           (int)L, (const cpx<T>*)s.tw[a], inverse, ss, (const double*)s.lam);
     return 0;
   };
-  SolveSpec off = s.ss;
+  SolveSpec off = s.ss, on = s.ss;
   off.active = 0;
-  const int d = g.d;
-  if (pass(0, rhs, 1, s.spec, 0, 1.0, 0, off)) return 1;
-  for (int a = 1; a < d - 1; ++a)
-    if (pass(a, s.spec, 0, s.spec, 0, 1.0, 0, off)) return 1;
-  SolveSpec on = s.ss;
   on.active = 1;
-  if (pass(d - 1, s.spec, 0, s.spec, 0, 1.0, 0, on)) return 1;
+  for (int a = 0; a < g.d; ++a) off.dims[a] = on.dims[a] = sg.dims[a];
+  const int d = g.d;
+  const unsigned eg = (unsigned)grid_for<T>(sg.N);
+  if (sg.half) {
+    if (pass(0, FFT_R2C, rhs, s.spec, 1.0, 0, off)) return 1;
+  } else {
+    launch("fft", k_real_to_cpx<T>, eg, kRedThreads, 0, st, rhs, s.spec, g.N);
+    if (pass(0, FFT_C2C, s.spec, s.spec, 1.0, 0, off)) return 1;
+  }
+  for (int a = 1; a < d - 1; ++a)
+    if (pass(a, FFT_C2C, s.spec, s.spec, 1.0, 0, off)) return 1;
+  if (pass(d - 1, FFT_C2C, s.spec, s.spec, 1.0, 0, on)) return 1;
   for (int a = d - 2; a >= 1; --a)
-    if (pass(a, s.spec, 0, s.spec, 0, 1.0, 1, off)) return 1;
-  if (pass(0, s.spec, 0, out, 1, 1.0 / (double)g.N, 1, off)) return 1;
+    if (pass(a, FFT_C2C, s.spec, s.spec, 1.0, 1, off)) return 1;
+  if (sg.half) {
+    // unnormalised inverses contribute (n0/2) prod_{a>0} n_a = N / 2
+    if (pass(0, FFT_C2R, s.spec, out, 2.0 / (double)g.N, 1, off)) return 1;
+  } else {
+    if (pass(0, FFT_C2C, s.spec, s.spec, 1.0, 1, off)) return 1;
+    launch("fft", k_cpx_to_real<T>, eg, kRedThreads, 0, st, (const cpx<T>*)s.spec, out, g.N,
+           1.0 / (double)g.N);
+  }
   TR_LAUNCH_CHECK();
   return 0;
 }
@@ -210,26 +268,42 @@ static int admm_step(Solver<T>& s, double* hout) {
     // noise and dual updates (solvers.py:239-246)
     const double level = s.cfg.lam / mu;
     const int structure = s.cfg.kind == 1 ? 3 : s.cfg.structure;
+    const double q0 = s.cfg.psi.p0, q1 = s.cfg.psi.p1;
     if (structure == 1 || structure == 2) {
       const int64_t face = g.dims[0] * g.dims[1];
-      if (structure == 1)
-        launch("group_scale", k_group_scale<T>, (unsigned)cdiv(face, 256), 256, 0, st, g, 1, s.A,
-               s.mask, (const T*)s.l, (const T*)s.y, mu, s.cfg.psi, level, s.scale);
-      else
-        launch("group_scale", k_group_scale<T>, (unsigned)(N / face), 256, 0, st, g, 2, s.A,
-               s.mask, (const T*)s.l, (const T*)s.y, mu, s.cfg.psi, level, s.scale);
+      const unsigned gg = (unsigned)(structure == 1 ? cdiv(face, 256) : N / face);
+#define TR_GS(K)                                                                             \
+  launch("group_scale", k_group_scale<T, K>, gg, 256, 0, st, g, structure, s.A, s.mask,     \
+         (const T*)s.l, (const T*)s.y, mu, q0, q1, level, s.scale)
+      TR_PEN_DISPATCH(s.cfg.psi.kind, TR_GS)
+#undef TR_GS
     }
-    launch("noise_dual", k_noise_dual<T>, grid, kRedThreads, 0, st, g, structure, s.A, s.mask,
-           (const T*)s.l, (const T*)s.lold, s.e, s.y, mu, s.cfg.psi, level,
-           (const double*)s.scale, part);
+#define TR_ND2(K, S)                                                                          \
+  launch("noise_dual", k_noise_dual<T, K, S>, grid, kRedThreads, 0, st, g, s.A, s.mask,      \
+         (const T*)s.l, (const T*)s.lold, s.e, s.y, mu, q0, q1, level, (const double*)s.scale, \
+         part)
+#define TR_ND(K)                            \
+  switch (structure) {                      \
+    case 0: TR_ND2(K, 0); break;            \
+    case 1: TR_ND2(K, 1); break;            \
+    case 2: TR_ND2(K, 2); break;            \
+    default: TR_ND2(K, 3); break;           \
+  }
+    TR_PEN_DISPATCH(s.cfg.psi.kind, TR_ND)
+#undef TR_ND
+#undef TR_ND2
     launch("final_reduce", k_final_reduce, 1, 256, 0, st, (const double*)part, (int)rb, 7,
            0b0010101u, res + 64);
   } else {
     // one-bit (onebit.py:171-192)
     const bool robust = s.cfg.kind == 3;
-    launch("onebit_fit", k_onebit_fit<T>, grid, kRedThreads, 0, st, N, s.A, s.B, s.cfg.mcount, mu,
-           (const T*)s.z, (const T*)s.y, s.cfg.alpha, (const T*)s.lold, s.l, s.e, robust ? 1 : 0,
-           s.cfg.psi, s.cfg.lam2, part);
+    const double q0 = s.cfg.psi.p0, q1 = s.cfg.psi.p1;
+#define TR_OF(K)                                                                               \
+  launch("onebit_fit", k_onebit_fit<T, K>, grid, kRedThreads, 0, st, N, s.A, s.B, s.cfg.mcount, \
+         mu, (const T*)s.z, (const T*)s.y, s.cfg.alpha, (const T*)s.lold, s.l, s.e,            \
+         robust ? 1 : 0, q0, q1, s.cfg.lam2, part)
+    TR_PEN_DISPATCH(s.cfg.psi.kind, TR_OF)
+#undef TR_OF
     launch("final_reduce", k_final_reduce, 1, 256, 0, st, (const double*)part, (int)rb, 3, 0b100u,
            res + 80);
     // Z-subproblem: solve with b = L + Y / mu

@@ -1,6 +1,12 @@
 // Elementwise / stencil kernels of the ADMM solvers (tenrec/solvers.py:204-284,
 // tenrec/onebit.py:141-220), each fused with the Eq. (24) residual reductions
-// it can produce from the values it already has in registers.
+// it can produce from the values it already holds.
+//
+// Kernels walk the tensor line by line (a line = the contiguous axis-0 fiber):
+// the multi-index of a line, and so the circular-neighbour offsets along the
+// other axes, is computed once per line, then the threads of the block stream
+// along the line (coalesced).  Penalty kinds are template parameters so each
+// instantiation carries only its own proximity operator.
 #pragma once
 
 #include "common.cuh"
@@ -18,12 +24,19 @@ struct Geom {
   int64_t N;
 };
 
-// index of the circular neighbour of i along axis a (dir = +1 next, -1 previous)
-__device__ __forceinline__ int64_t nbr(int64_t i, const Geom& g, int a, int dir) {
+// offsets of the previous / next element along axis a (a >= 1) for a line
+// whose axis-a coordinate is j
+__device__ __forceinline__ void axis_offsets(const Geom& g, int a, int64_t j, int64_t& prev,
+                                             int64_t& next) {
   const int64_t n = g.dims[a], s = g.st[a];
-  const int64_t j = (i / s) % n;
-  if (dir > 0) return j + 1 < n ? i + s : i - s * (n - 1);
-  return j > 0 ? i - s : i + s * (n - 1);
+  prev = j > 0 ? -s : s * (n - 1);
+  next = j + 1 < n ? s : -s * (n - 1);
+}
+
+// coordinate of the line (index of axes 1..d-1 flattened) along axis a >= 1
+__device__ __forceinline__ int64_t line_coord(const Geom& g, int64_t line, int a) {
+  const int64_t lst = g.st[a] / g.dims[0];
+  return (line / lst) % g.dims[a];
 }
 
 template <typename T>
@@ -32,6 +45,12 @@ struct ModePtrs {
   int axis[kMaxOrder];  // -1 = identity chain (pure low-rank ablation)
   T* p[kMaxOrder];
 };
+
+template <int KIND>
+__device__ __forceinline__ double prox_k(double p0, double p1, double mu, double v) {
+  Penalty pen{KIND, p0, p1};
+  return prox(pen, mu, v);
+}
 
 // per-block partial reductions: NQ values, `is_max` bitmask selects max vs sum
 template <int NQ>
@@ -62,41 +81,72 @@ __global__ void k_final_reduce(const double* __restrict__ part, int nblocks, int
 //   b = A - B + y / mu ;  rhs = b + sum_k D_k^T (g_k - lag_k / mu)
 // pure low-rank chain: out = 0.5 * (b + g - lag / mu)  (solvers.py:194-195), the final L.
 template <typename T>
-__global__ void k_admm_rhs(Geom g, const T* __restrict__ A, const T* __restrict__ B,
-                           const T* __restrict__ y, double mu, ModePtrs<T> gm, ModePtrs<T> lag,
-                           T* __restrict__ out) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.N; i += stride) {
-    const T bv = (B ? (A[i] - B[i]) : A[i]) + y[i] / (T)mu;
-    if (gm.count == 1 && gm.axis[0] < 0) {
-      out[i] = (T)0.5 * (bv + (gm.p[0][i] - lag.p[0][i] / (T)mu));
-      continue;
+__global__ void __launch_bounds__(kRedThreads) k_admm_rhs(Geom g, const T* __restrict__ A,
+                                                          const T* __restrict__ B,
+                                                          const T* __restrict__ y, double mu,
+                                                          ModePtrs<T> gm, ModePtrs<T> lag,
+                                                          T* __restrict__ out) {
+  const int64_t n0 = g.dims[0], lines = g.N / n0;
+  const T imu = T(1) / (T)mu;
+  const bool pure = gm.count == 1 && gm.axis[0] < 0;
+  for (int64_t line = blockIdx.x; line < lines; line += gridDim.x) {
+    int64_t prevoff[kMaxOrder];
+#pragma unroll
+    for (int k = 0; k < kMaxOrder; ++k) {
+      prevoff[k] = 0;
+      if (k < gm.count && gm.axis[k] > 0) {
+        int64_t nx;
+        axis_offsets(g, gm.axis[k], line_coord(g, line, gm.axis[k]), prevoff[k], nx);
+      }
     }
-    T acc = bv;
-    for (int k = 0; k < gm.count; ++k) {
-      const int a = gm.axis[k];
-      const int64_t ip = nbr(i, g, a, -1);
-      const T gi = gm.p[k][i] - lag.p[k][i] / (T)mu;
-      const T gp = gm.p[k][ip] - lag.p[k][ip] / (T)mu;
-      acc += gp - gi;
+    const int64_t base = line * n0;
+    for (int64_t i0 = threadIdx.x; i0 < n0; i0 += blockDim.x) {
+      const int64_t i = base + i0;
+      const T bv = (B ? (A[i] - B[i]) : A[i]) + y[i] / (T)mu;
+      if (pure) {
+        out[i] = (T)0.5 * (bv + (gm.p[0][i] - lag.p[0][i] / (T)mu));
+        continue;
+      }
+      T acc = bv;
+#pragma unroll
+      for (int k = 0; k < kMaxOrder; ++k) {
+        if (k < gm.count) {
+          const int a = gm.axis[k];
+          const int64_t ip = a == 0 ? base + (i0 > 0 ? i0 - 1 : n0 - 1) : i + prevoff[k];
+          const T gi = gm.p[k][i] - lag.p[k][i] / (T)mu;
+          const T gp = gm.p[k][ip] - lag.p[k][ip] / (T)mu;
+          acc += gp - gi;
+        }
+      }
+      out[i] = acc;
     }
-    out[i] = acc;
   }
+  (void)imu;
 }
 
-// LRTA input of mode k: X = D_k L + lag_k / mu (identity chain: L + lag / mu)
+// LRTA input of mode `axis`: X = D_axis L + lag / mu (identity chain: L + lag / mu)
 template <typename T>
-__global__ void k_lrta_input(Geom g, const T* __restrict__ l, int axis, const T* __restrict__ lag,
-                             double mu, T* __restrict__ X) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.N; i += stride) {
-    const T gl = axis < 0 ? l[i] : l[nbr(i, g, axis, +1)] - l[i];
-    X[i] = gl + lag[i] / (T)mu;
+__global__ void __launch_bounds__(kRedThreads) k_lrta_input(Geom g, const T* __restrict__ l,
+                                                            int axis, const T* __restrict__ lag,
+                                                            double mu, T* __restrict__ X) {
+  const int64_t n0 = g.dims[0], lines = g.N / n0;
+  for (int64_t line = blockIdx.x; line < lines; line += gridDim.x) {
+    int64_t pv = 0, nx = 0;
+    if (axis > 0) axis_offsets(g, axis, line_coord(g, line, axis), pv, nx);
+    const int64_t base = line * n0;
+    for (int64_t i0 = threadIdx.x; i0 < n0; i0 += blockDim.x) {
+      const int64_t i = base + i0;
+      T gl;
+      if (axis < 0) gl = l[i];
+      else if (axis == 0) gl = l[base + (i0 + 1 < n0 ? i0 + 1 : 0)] - l[i];
+      else gl = l[i + nx] - l[i];
+      X[i] = gl + lag[i] / (T)mu;
+    }
   }
 }
 
-// multiplier update of mode k (solvers.py:247-248) with its residuals:
-//   lag += mu (D_k L - G_new);  partial q: 0 max|DL-G|, 1 sum (DL-G)^2,
+// multiplier update of one mode (solvers.py:247-248) with its residuals:
+//   lag += mu (D L - G_new);  partial q: 0 max|DL-G|, 1 sum (DL-G)^2,
 //   2 max|G_new-G_old|, 3 sum (G_new-G_old)^2, 4 sum lag_new^2
 template <typename T>
 __global__ void __launch_bounds__(kRedThreads) k_lag_update(Geom g, const T* __restrict__ l, int axis,
@@ -106,19 +156,28 @@ __global__ void __launch_bounds__(kRedThreads) k_lag_update(Geom g, const T* __r
                                                             double* __restrict__ part) {
   __shared__ double red[32];
   double v[5] = {0, 0, 0, 0, 0};
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.N; i += stride) {
-    const T gl = axis < 0 ? l[i] : l[nbr(i, g, axis, +1)] - l[i];
-    const T gn = gnew[i];
-    const T gap = gl - gn;
-    const T ln = lag[i] + (T)mu * gap;
-    lag[i] = ln;
-    const double dg = (double)gn - (double)gold[i];
-    v[0] = fmax(v[0], fabs((double)gap));
-    v[1] += (double)gap * (double)gap;
-    v[2] = fmax(v[2], fabs(dg));
-    v[3] += dg * dg;
-    v[4] += (double)ln * (double)ln;
+  const int64_t n0 = g.dims[0], lines = g.N / n0;
+  for (int64_t line = blockIdx.x; line < lines; line += gridDim.x) {
+    int64_t pv = 0, nx = 0;
+    if (axis > 0) axis_offsets(g, axis, line_coord(g, line, axis), pv, nx);
+    const int64_t base = line * n0;
+    for (int64_t i0 = threadIdx.x; i0 < n0; i0 += blockDim.x) {
+      const int64_t i = base + i0;
+      T gl;
+      if (axis < 0) gl = l[i];
+      else if (axis == 0) gl = l[base + (i0 + 1 < n0 ? i0 + 1 : 0)] - l[i];
+      else gl = l[i + nx] - l[i];
+      const T gn = gnew[i];
+      const T gap = gl - gn;
+      const T ln = lag[i] + (T)mu * gap;
+      lag[i] = ln;
+      const double dg = (double)gn - (double)gold[i];
+      v[0] = fmax(v[0], fabs((double)gap));
+      v[1] += (double)gap * (double)gap;
+      v[2] = fmax(v[2], fabs(dg));
+      v[3] += dg * dg;
+      v[4] += (double)ln * (double)ln;
+    }
   }
   block_partials<5>(v, 0b00101u, red, part);
 }
@@ -126,11 +185,11 @@ __global__ void __launch_bounds__(kRedThreads) k_lag_update(Geom g, const T* __r
 // group scales of the structured noise shrinkage (shrink.py:49-54) of
 // mask * h, h = mobs - l + y / mu:  scale = prox(level, ||group||) / ||group||.
 // structure 1 = tube (i0, i1) over trailing modes, 2 = slice (face) over (i0, i1).
-template <typename T>
+template <typename T, int KIND>
 __global__ void k_group_scale(Geom g, int structure, const T* __restrict__ mobs,
                               const uint8_t* __restrict__ mask, const T* __restrict__ l,
-                              const T* __restrict__ y, double mu, Penalty pen, double level,
-                              double* __restrict__ scale) {
+                              const T* __restrict__ y, double mu, double p0, double p1,
+                              double level, double* __restrict__ scale) {
   const int64_t face = g.dims[0] * g.dims[1];
   const int64_t nf = g.N / face;
   if (structure == 1) {
@@ -143,7 +202,7 @@ __global__ void k_group_scale(Geom g, int structure, const T* __restrict__ mobs,
       s2 += h * h;
     }
     const double gn = sqrt(s2);
-    scale[t] = gn > 0 ? prox(pen, level, gn) / gn : 0.0;
+    scale[t] = gn > 0 ? prox_k<KIND>(p0, p1, level, gn) / gn : 0.0;
   } else {
     __shared__ double red[32];
     const int64_t f = blockIdx.x;
@@ -154,7 +213,7 @@ __global__ void k_group_scale(Geom g, int structure, const T* __restrict__ mobs,
       s2 += h * h;
     }
     const double gn = sqrt(block_sum(s2, red));
-    if (threadIdx.x == 0) scale[f] = gn > 0 ? prox(pen, level, gn) / gn : 0.0;
+    if (threadIdx.x == 0) scale[f] = gn > 0 ? prox_k<KIND>(p0, p1, level, gn) / gn : 0.0;
   }
 }
 
@@ -162,56 +221,84 @@ __global__ void k_group_scale(Geom g, int structure, const T* __restrict__ mobs,
 //   h = mobs - l + y/mu ; E = mask*shrink(mask*h) + (1-mask)*h ; y += mu (mobs - l - E)
 //   structure 0 entry / 1 tube / 2 slice / 3 noise-free (E = 0 on the mask)
 //   partial q: 0 max|l-lold| 1 sum 2 max|E-Eold| 3 sum 4 max|fit| 5 sum 6 sum y^2
-template <typename T>
-__global__ void __launch_bounds__(kRedThreads) k_noise_dual(Geom g, int structure,
-                                                            const T* __restrict__ mobs,
+// Prox in the streaming precision for the closed-form families (l1, firm,
+// mcp, scad); the iterative / candidate families (lq, capped-lq, log) stay fp64.
+template <int KIND, typename T>
+__device__ __forceinline__ T prox_t(T p0, double p0d, double p1d, T mu, double mud, T v) {
+  if (KIND <= 3) {
+    if (mu == T(0)) return v;
+    const T a = v < T(0) ? -v : v;
+    T r;
+    if (KIND == 0) {
+      r = a > mu ? a - mu : T(0);
+    } else if (KIND == 1 || KIND == 2) {
+      r = a <= mu ? T(0) : (a < p0 * mu ? p0 * (a - mu) / (p0 - T(1)) : a);
+    } else {
+      r = a <= T(2) * mu ? (a > mu ? a - mu : T(0))
+                         : (a <= p0 * mu ? ((p0 - T(1)) * a - p0 * mu) / (p0 - T(2)) : a);
+    }
+    return v > T(0) ? r : (v < T(0) ? -r : T(0));
+  } else {
+    return (T)prox_k<KIND>(p0d, p1d, mud, (double)v);
+  }
+}
+
+// STRUCT: 0 entry, 1 tube, 2 slice, 3 noise-free (E = 0 on the mask)
+template <typename T, int KIND, int STRUCT>
+__global__ void __launch_bounds__(kRedThreads) k_noise_dual(Geom g, const T* __restrict__ mobs,
                                                             const uint8_t* __restrict__ mask,
                                                             const T* __restrict__ l,
                                                             const T* __restrict__ lold,
                                                             T* __restrict__ e, T* __restrict__ y,
-                                                            double mu, Penalty pen, double level,
+                                                            double mu, double p0, double p1,
+                                                            double level,
                                                             const double* __restrict__ scale,
                                                             double* __restrict__ part) {
   __shared__ double red[32];
-  double v[7] = {0, 0, 0, 0, 0, 0, 0};
+  // per-thread partials in T (fp32 sums over <= a few hundred elements), per-block fp64
+  T v[7] = {T(0), T(0), T(0), T(0), T(0), T(0), T(0)};
   const int64_t face = g.dims[0] * g.dims[1];
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const T tmu = (T)mu, tlev = (T)level, tp0 = (T)p0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.N; i += stride) {
-    const T mi = mobs[i], li = l[i], yi = y[i];
-    const T h = mi - li + yi / (T)mu;
+    const T mi = mobs[i], li = l[i], yi = y[i], eo = e[i], lo = lold[i];
+    const bool obs = mask[i] != 0;
+    const T h = mi - li + yi / tmu;
     T en;
-    if (!mask[i]) {
+    if (!obs) {
       en = h;
-    } else if (structure == 3) {
+    } else if (STRUCT == 3) {
       en = T(0);
-    } else if (structure == 0) {
-      en = (T)prox(pen, level, (double)h);
+    } else if (STRUCT == 0) {
+      en = prox_t<KIND, T>(tp0, p0, p1, tlev, level, h);
     } else {
-      const double sc = structure == 1 ? scale[i % face] : scale[i / face];
+      const double sc = STRUCT == 1 ? scale[i % face] : scale[i / face];
       en = (T)((double)h * sc);
     }
     const T fit = mi - li - en;
-    const T yn = yi + (T)mu * fit;
-    const double dl = (double)li - (double)lold[i];
-    const double de = (double)en - (double)e[i];
+    const T yn = yi + tmu * fit;
     e[i] = en;
     y[i] = yn;
+    const T dl = li - lo, de = en - eo;
     v[0] = fmax(v[0], fabs(dl));
     v[1] += dl * dl;
     v[2] = fmax(v[2], fabs(de));
     v[3] += de * de;
-    v[4] = fmax(v[4], fabs((double)fit));
-    v[5] += (double)fit * (double)fit;
-    v[6] += (double)yn * (double)yn;
+    v[4] = fmax(v[4], fabs(fit));
+    v[5] += fit * fit;
+    v[6] += yn * yn;
   }
-  block_partials<7>(v, 0b0010101u, red, part);
+  double vd[7];
+#pragma unroll
+  for (int q = 0; q < 7; ++q) vd[q] = (double)v[q];
+  block_partials<7>(vd, 0b0010101u, red, part);
 }
 
 // one-bit data-fit update (onebit.py:128-138, 172-180):
 //   L = clip((J1 + m mu Z - m Y [- J2 S]) / (J2 + m mu), -alpha, alpha)
 //   robust: S = observed ? prox(lam2 m / c, J1/c - L) : 0   (c = J2)
 //   partial q: 0 sum (L-Lold)^2  1 sum Lold^2  2 max|L-Lold|
-template <typename T>
+template <typename T, int KIND>
 __global__ void __launch_bounds__(kRedThreads) k_onebit_fit(int64_t N, const T* __restrict__ j1,
                                                             const T* __restrict__ j2, double m,
                                                             double mu, const T* __restrict__ z,
@@ -219,7 +306,7 @@ __global__ void __launch_bounds__(kRedThreads) k_onebit_fit(int64_t N, const T* 
                                                             const T* __restrict__ lold,
                                                             T* __restrict__ lnew,
                                                             T* __restrict__ s, int robust,
-                                                            Penalty psi, double lam2,
+                                                            double p0, double p1, double lam2,
                                                             double* __restrict__ part) {
   __shared__ double red[32];
   double v[3] = {0, 0, 0};
@@ -235,7 +322,7 @@ __global__ void __launch_bounds__(kRedThreads) k_onebit_fit(int64_t N, const T* 
       T sn = T(0);
       if (c > T(0)) {
         const T w = j1[i] / (c > T(1) ? c : T(1)) - ln;
-        sn = (T)prox(psi, lam2 * m / (double)c, (double)w);
+        sn = (T)prox_k<KIND>(p0, p1, lam2 * m / (double)c, (double)w);
       }
       s[i] = sn;
     }
@@ -267,12 +354,6 @@ __global__ void __launch_bounds__(kRedThreads) k_onebit_dual(int64_t N, const T*
   block_partials<2>(v, 0b01u, red, part);
 }
 
-template <typename T>
-__global__ void k_fill(T* __restrict__ p, int64_t n, T v) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) p[i] = v;
-}
-
 // real T <-> fp64 (deterministic small-face t-SVT path)
 template <typename A, typename B>
 __global__ void k_convert(const A* __restrict__ in, B* __restrict__ out, int64_t n) {
@@ -280,5 +361,17 @@ __global__ void k_convert(const A* __restrict__ in, B* __restrict__ out, int64_t
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
     out[i] = (B)in[i];
 }
+
+// launch a KIND-templated kernel for a runtime penalty kind
+#define TR_PEN_DISPATCH(kind, CALL) \
+  switch (kind) {                   \
+    case 0: CALL(0); break;         \
+    case 1: CALL(1); break;         \
+    case 2: CALL(2); break;         \
+    case 3: CALL(3); break;         \
+    case 4: CALL(4); break;         \
+    case 5: CALL(5); break;         \
+    default: CALL(6); break;        \
+  }
 
 }  // namespace tr

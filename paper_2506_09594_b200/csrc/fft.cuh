@@ -7,9 +7,13 @@
 // Layout: element (lo, k, hi) of an axis of length n with lo-stride st lives at
 // lo + st * (k + n * hi).  One CTA loads a tile of `L` lines (consecutive lo
 // when st > 1 for coalescing, consecutive hi when the axis is contiguous) into
-// shared memory, transforms every line there (radix-2 DIT for powers of two,
-// direct DFT otherwise), and writes it back.  The last-axis pass of the solve
-// does forward FFT -> divide -> inverse FFT without leaving shared memory.
+// shared memory and transforms every line there:
+//   * powers of two: radix-4 Stockham autosort (radix-2 last stage when log2 n
+//     is odd), each thread holding its groups in registers, twiddles in smem;
+//   * other lengths: direct DFT.
+// Axis 0 is real-to-complex on the way in (n0/2+1 bins, the conjugate-even half
+// spectrum of a real tensor) and complex-to-real on the way out.  The last-axis
+// pass of the solve does forward FFT -> divide -> inverse FFT in shared memory.
 #pragma once
 
 #include "common.cuh"
@@ -29,6 +33,8 @@ template <typename T>
 __device__ __forceinline__ cpx<T> cmulc(cpx<T> a, cpx<T> b) {
   return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re};
 }
+template <typename T>
+__device__ __forceinline__ cpx<T> cconjt(cpx<T> a) { return {a.re, -a.im}; }
 
 // tw[k] = exp(-2 pi i k / n), k < n, computed in fp64 with exact argument reduction
 template <typename T>
@@ -41,115 +47,267 @@ __global__ void k_twiddles(int n, cpx<T>* __restrict__ tw) {
 }
 
 struct SolveSpec {
-  int active;          // last-axis pass of the diagonal solve
-  int d;               // tensor order
-  int64_t dims[10];
-  int64_t lam_off[10];  // offset of axis k's 4 sin^2(pi j / n_k) table in lam, -1 if k not in Gamma
+  int active;           // last-axis pass of the diagonal solve
+  int d;                // tensor order
+  int64_t dims[10];     // spectrum dims (axis 0 = n0/2+1 in the half-spectrum layout)
+  int64_t lam_off[10];  // offset of axis k's 4 sin^2(pi j / n_k) table, -1 if k not in Gamma
 };
 
-__device__ __forceinline__ int brev(int x, int bits) { return (int)(__brev((unsigned)x) >> (32 - bits)); }
-
-// in-place transform of the L lines held in shared memory; element (l, k) at l*ls + k*ks
-template <typename T>
-__device__ void smem_lines_fft(cpx<T>* buf, cpx<T>* tmp, int L, int n, int64_t ls, int64_t ks,
-                               const cpx<T>* __restrict__ tw, bool inverse, bool pow2, int bits) {
-  const int nt = blockDim.x;
-  if (n == 1) return;
-  if (pow2) {
-    // bit-reversal permutation (swap pairs once)
-    for (int e = threadIdx.x; e < L * n; e += nt) {
-      const int l = e / n, k = e % n;
-      const int r = brev(k, bits);
-      if (r > k) {
-        const cpx<T> a = buf[l * ls + k * ks];
-        buf[l * ls + k * ks] = buf[l * ls + r * ks];
-        buf[l * ls + r * ks] = a;
+// Stockham radix-4/2 FFT of the L lines in smem (element (l, k) at l*ls + k*ks),
+// in place: every stage reads all groups into registers, syncs, writes.
+// twiddles: ts[m] = exp(-2 pi i m / n) for m < n (smem); inverse conjugates.
+template <typename T, int GMAX>
+__device__ void stockham_lines(cpx<T>* buf, int L, int n, int64_t ls, int64_t ks,
+                               const cpx<T>* ts, bool inverse, bool lo_major) {
+  int Ns = 1;
+  while (Ns < n) {
+    const int R = (n / Ns) % 4 == 0 ? 4 : 2;
+    const int groups = n / R;
+    const int total = L * groups;
+    cpx<T> v[GMAX][4];
+    int cnt = 0;
+    // load phase
+#pragma unroll
+    for (int g = 0; g < GMAX; ++g) {
+      const int e = threadIdx.x + g * blockDim.x;
+      if (e < total) {
+        const int l = lo_major ? e % L : e / groups;
+        const int j = lo_major ? e / L : e % groups;
+        const int jm = j % Ns;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          if (r < R) {
+            cpx<T> x = buf[l * ls + (int64_t)(j + r * groups) * ks];
+            if (r > 0 && jm > 0) {
+              cpx<T> w = ts[(jm * r * (n / (Ns * R))) % n];
+              if (inverse) w.im = -w.im;
+              x = cmulc(x, w);
+            }
+            v[g][r] = x;
+          }
+        }
+        cnt = g + 1;
       }
     }
     __syncthreads();
-    for (int len = 2; len <= n; len <<= 1) {
-      const int half = len >> 1, step = n / len;
-      for (int e = threadIdx.x; e < L * (n >> 1); e += nt) {
-        const int l = e / (n >> 1), b = e % (n >> 1);
-        const int i = (b / half) * len + (b % half), j = i + half;
-        cpx<T> w = tw[(b % half) * step];
-        if (inverse) w.im = -w.im;
-        const cpx<T> t = cmulc(w, buf[l * ls + j * ks]);
-        const cpx<T> u = buf[l * ls + i * ks];
-        buf[l * ls + i * ks] = cadd(u, t);
-        buf[l * ls + j * ks] = csub(u, t);
+#pragma unroll
+    for (int g = 0; g < GMAX; ++g) {
+      if (g < cnt) {
+        const int e = threadIdx.x + g * blockDim.x;
+        const int l = lo_major ? e % L : e / groups;
+        const int j = lo_major ? e / L : e % groups;
+        const int jm = j % Ns;
+        const int64_t base = (int64_t)((j / Ns) * Ns * R + jm);
+        if (R == 4) {
+          const cpx<T> a0 = cadd(v[g][0], v[g][2]), a1 = csub(v[g][0], v[g][2]);
+          const cpx<T> a2 = cadd(v[g][1], v[g][3]);
+          const cpx<T> d = csub(v[g][1], v[g][3]);
+          // forward: a3 = -i d ; inverse: +i d
+          const cpx<T> a3 = inverse ? cpx<T>{-d.im, d.re} : cpx<T>{d.im, -d.re};
+          buf[l * ls + (base + 0 * Ns) * ks] = cadd(a0, a2);
+          buf[l * ls + (base + 1 * Ns) * ks] = cadd(a1, a3);
+          buf[l * ls + (base + 2 * Ns) * ks] = csub(a0, a2);
+          buf[l * ls + (base + 3 * Ns) * ks] = csub(a1, a3);
+        } else {
+          buf[l * ls + (base + 0 * Ns) * ks] = cadd(v[g][0], v[g][1]);
+          buf[l * ls + (base + 1 * Ns) * ks] = csub(v[g][0], v[g][1]);
+        }
       }
-      __syncthreads();
-    }
-  } else {
-    // direct DFT through tmp (same shape as buf)
-    for (int e = threadIdx.x; e < L * n; e += nt) {
-      const int l = e / n, k = e % n;
-      cpx<T> acc = {T(0), T(0)};
-      int idx = 0;
-      for (int j = 0; j < n; ++j) {
-        cpx<T> w = tw[idx];
-        if (inverse) w.im = -w.im;
-        acc = cadd(acc, cmulc(w, buf[l * ls + j * ks]));
-        idx += k;
-        if (idx >= n) idx -= n;
-      }
-      tmp[l * ls + k * ks] = acc;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < L * n; e += nt) {
-      const int l = e / n, k = e % n;
-      buf[l * ls + k * ks] = tmp[l * ls + k * ks];
-    }
-    __syncthreads();
+    Ns *= R;
   }
 }
 
-// One pass along an axis.  in_real: input is real T; out_real: write Re * out_scale.
+// Shift/mask version of stockham_lines for power-of-two L and n (lL = log2 L,
+// ln = log2 n) with 32-bit shared-memory indices: no integer division in the
+// butterfly loops.  Layout: lo_major -> element (l, k) at (k << lL) + l,
+// otherwise (l << ln) + k.
+template <typename T, int GMAX>
+__device__ void stockham_p2(cpx<T>* buf, int lL, int ln, const cpx<T>* ts, bool inverse,
+                            bool lo_major) {
+  const int n = 1 << ln;
+  int lNs = 0;
+  while (lNs < ln) {
+    const int lR = (ln - lNs) >= 2 ? 2 : 1;
+    const int lg = ln - lR;  // log2(groups)
+    const int total = 1 << (lL + lg);
+    const int tws = ln - lNs - lR;  // log2(n / (Ns R))
+    const int nsm = (1 << lNs) - 1;
+    cpx<T> v[GMAX][4];
+#pragma unroll
+    for (int g = 0; g < GMAX; ++g) {
+      const int e = threadIdx.x + g * blockDim.x;
+      if (e < total) {
+        const int l = lo_major ? (e & ((1 << lL) - 1)) : (e >> lg);
+        const int j = lo_major ? (e >> lL) : (e & ((1 << lg) - 1));
+        const int jm = j & nsm;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          if (r < (1 << lR)) {
+            const int k = j + (r << lg);
+            cpx<T> x = buf[lo_major ? (k << lL) + l : (l << ln) + k];
+            if (r > 0 && jm > 0) {
+              cpx<T> w = ts[(jm * r) << tws];
+              if (inverse) w.im = -w.im;
+              x = cmulc(x, w);
+            }
+            v[g][r] = x;
+          }
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int g = 0; g < GMAX; ++g) {
+      const int e = threadIdx.x + g * blockDim.x;
+      if (e < total) {
+        const int l = lo_major ? (e & ((1 << lL) - 1)) : (e >> lg);
+        const int j = lo_major ? (e >> lL) : (e & ((1 << lg) - 1));
+        const int base = ((j >> lNs) << (lNs + lR)) + (j & nsm);
+        auto at = [&](int r) -> cpx<T>& {
+          const int k = base + (r << lNs);
+          return buf[lo_major ? (k << lL) + l : (l << ln) + k];
+        };
+        if (lR == 2) {
+          const cpx<T> a0 = cadd(v[g][0], v[g][2]), a1 = csub(v[g][0], v[g][2]);
+          const cpx<T> a2 = cadd(v[g][1], v[g][3]);
+          const cpx<T> d = csub(v[g][1], v[g][3]);
+          const cpx<T> a3 = inverse ? cpx<T>{-d.im, d.re} : cpx<T>{d.im, -d.re};
+          at(0) = cadd(a0, a2);
+          at(1) = cadd(a1, a3);
+          at(2) = csub(a0, a2);
+          at(3) = csub(a1, a3);
+        } else {
+          at(0) = cadd(v[g][0], v[g][1]);
+          at(1) = csub(v[g][0], v[g][1]);
+        }
+      }
+    }
+    __syncthreads();
+    lNs += lR;
+  }
+  (void)n;
+}
+
+// direct DFT of the lines (non power-of-two n), result back into buf via tmp
 template <typename T>
-__global__ void __launch_bounds__(256) k_fft_axis(const void* __restrict__ in, int in_real,
-                                                  void* __restrict__ out, int out_real,
-                                                  double out_scale, int64_t st, int n, int64_t hi,
-                                                  int L, const cpx<T>* __restrict__ tw, int inverse,
+__device__ void direct_lines(cpx<T>* buf, cpx<T>* tmp, int L, int n, int64_t ls, int64_t ks,
+                             const cpx<T>* ts, bool inverse) {
+  for (int e = threadIdx.x; e < L * n; e += blockDim.x) {
+    const int l = e / n, k = e % n;
+    cpx<T> acc = {T(0), T(0)};
+    int idx = 0;
+    for (int j = 0; j < n; ++j) {
+      cpx<T> w = ts[idx];
+      if (inverse) w.im = -w.im;
+      acc = cadd(acc, cmulc(w, buf[l * ls + (int64_t)j * ks]));
+      idx += k;
+      if (idx >= n) idx -= n;
+    }
+    tmp[l * ls + (int64_t)k * ks] = acc;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < L * n; e += blockDim.x) {
+    const int l = e / n, k = e % n;
+    buf[l * ls + (int64_t)k * ks] = tmp[l * ls + (int64_t)k * ks];
+  }
+  __syncthreads();
+}
+
+template <typename T>
+__device__ __forceinline__ void lines_fft(cpx<T>* buf, cpx<T>* tmp, int L, int n, int64_t ls,
+                                          int64_t ks, const cpx<T>* ts, bool inverse,
+                                          bool lo_major) {
+  if (n == 1) return;
+  if ((n & (n - 1)) == 0) {
+    // host guarantees L * n <= 16 * blockDim.x, i.e. <= 8 radix-2 groups per thread
+    stockham_lines<T, 8>(buf, L, n, ls, ks, ts, inverse, lo_major);
+  } else {
+    direct_lines<T>(buf, tmp, L, n, ls, ks, ts, inverse);
+  }
+}
+
+// Pass modes
+enum FftMode { FFT_C2C = 0, FFT_R2C = 1, FFT_C2R = 2 };
+
+// One pass along an axis.
+//  C2C: complex in/out, axis length n (lo-stride st, hi lines).
+//  R2C (axis 0 only, n = n0 even, hn = n/2): real input lines of n, complex
+//       output lines of hn+1 (half spectrum, contiguous).
+//  C2R (axis 0 only): inverse of R2C, real output times out_scale.
+// `ss.active` (C2C on the last axis): forward, divide, inverse.
+template <typename T>
+__global__ void __launch_bounds__(256) k_fft_axis(const void* __restrict__ in, void* __restrict__ out,
+                                                  int mode, double out_scale, int64_t st, int n,
+                                                  int64_t hi, int L,
+                                                  const cpx<T>* __restrict__ tw, int inverse,
                                                   SolveSpec ss, const double* __restrict__ lam) {
   extern __shared__ __align__(16) unsigned char fft_smem[];
-  cpx<T>* buf = reinterpret_cast<cpx<T>*>(fft_smem);
-  const bool pow2 = (n & (n - 1)) == 0;
-  cpx<T>* tmp = buf + (size_t)L * n;
-  int bits = 0;
-  while ((1 << bits) < n) ++bits;
-  // line l of this CTA -> (lo, hi)
+  // the transformed length (complex) and the element counts of in/out lines
+  const int nt = (mode == FFT_C2C) ? n : n / 2;
+  cpx<T>* ts = reinterpret_cast<cpx<T>*>(fft_smem);                 // nt twiddles
+  cpx<T>* buf = ts + nt;                                             // L x nt
+  cpx<T>* tmp = buf + (size_t)L * nt;                                // L x nt (non pow2)
+  for (int m = threadIdx.x; m < nt; m += blockDim.x)
+    ts[m] = tw[(mode == FFT_C2C) ? m : 2 * m];  // n-point table, even entries = nt-point
   int64_t lo0, hi0;
-  bool lo_lines;
-  if (st == 1) {
-    lo_lines = false;
+  const bool lo_lines = st > 1;
+  if (!lo_lines) {
     lo0 = 0;
     hi0 = (int64_t)blockIdx.x * L;
   } else {
-    lo_lines = true;
     const int64_t nlob = (st + L - 1) / L;
     lo0 = (int64_t)(blockIdx.x % nlob) * L;
     hi0 = blockIdx.x / nlob;
   }
-  // smem layout: lo-lines -> [k][l] (coalesced along lo), hi-lines -> [l][k]
-  const int64_t ls = lo_lines ? 1 : n, ks = lo_lines ? L : 1;
-  for (int e = threadIdx.x; e < L * n; e += blockDim.x) {
-    int l, k;
-    if (lo_lines) { l = e % L; k = e / L; } else { l = e / n; k = e % n; }
-    const int64_t lo = lo_lines ? lo0 + l : 0;
-    const int64_t hh = lo_lines ? hi0 : hi0 + l;
-    cpx<T> v = {T(0), T(0)};
-    if (lo < st && hh < hi) {
-      const int64_t g = lo + st * (k + (int64_t)n * hh);
-      if (in_real) v.re = reinterpret_cast<const T*>(in)[g];
-      else v = reinterpret_cast<const cpx<T>*>(in)[g];
+  const int64_t ls = lo_lines ? 1 : nt, ks = lo_lines ? L : 1;
+  const int hn = n / 2;
+  // ---- load ----
+  if (mode == FFT_R2C) {
+    // z[k] = x[2k] + i x[2k+1]
+    for (int e = threadIdx.x; e < L * nt; e += blockDim.x) {
+      const int l = e / nt, k = e % nt;
+      const int64_t line = hi0 + l;
+      cpx<T> v = {T(0), T(0)};
+      if (line < hi) {
+        const T* x = reinterpret_cast<const T*>(in) + line * n;
+        v = {x[2 * k], x[2 * k + 1]};
+      }
+      buf[l * ls + k * ks] = v;
     }
-    buf[l * ls + k * ks] = v;
+  } else if (mode == FFT_C2R) {
+    // Z[k] = E[k] + i O[k],  E = (X[k] + conj X[h-k]) / 2,  O = w^-k (X[k] - conj X[h-k]) / 2
+    for (int e = threadIdx.x; e < L * nt; e += blockDim.x) {
+      const int l = e / nt, k = e % nt;
+      const int64_t line = hi0 + l;
+      cpx<T> v = {T(0), T(0)};
+      if (line < hi) {
+        const cpx<T>* X = reinterpret_cast<const cpx<T>*>(in) + line * (hn + 1);
+        const cpx<T> a = X[k], b = cconjt(X[hn - k]);
+        const cpx<T> E = {(a.re + b.re) * T(0.5), (a.im + b.im) * T(0.5)};
+        cpx<T> w = tw[k];  // n-point twiddle e^{-2 pi i k / n}; need w^{-k} = conj
+        w.im = -w.im;
+        const cpx<T> D = {(a.re - b.re) * T(0.5), (a.im - b.im) * T(0.5)};
+        const cpx<T> O = cmulc(D, w);
+        v = {E.re - O.im, E.im + O.re};  // E + i O
+      }
+      buf[l * ls + k * ks] = v;
+    }
+  } else {
+    for (int e = threadIdx.x; e < L * nt; e += blockDim.x) {
+      int l, k;
+      if (lo_lines) { l = e % L; k = e / L; } else { l = e / nt; k = e % nt; }
+      const int64_t lo = lo_lines ? lo0 + l : 0;
+      const int64_t hh = lo_lines ? hi0 : hi0 + l;
+      cpx<T> v = {T(0), T(0)};
+      if (lo < st && hh < hi) v = reinterpret_cast<const cpx<T>*>(in)[lo + st * (k + (int64_t)n * hh)];
+      buf[l * ls + k * ks] = v;
+    }
   }
   __syncthreads();
-  smem_lines_fft<T>(buf, tmp, L, n, ls, ks, tw, inverse != 0, pow2, bits);
+  lines_fft<T>(buf, tmp, L, nt, ls, ks, ts, (mode == FFT_C2R) || inverse != 0, lo_lines);
   if (ss.active) {
-    // divide by 1 + sum_k lam_k(j_k); the transformed axis is the last one
     for (int e = threadIdx.x; e < L * n; e += blockDim.x) {
       int l, k;
       if (lo_lines) { l = e % L; k = e / L; } else { l = e / n; k = e % n; }
@@ -163,24 +321,413 @@ __global__ void __launch_bounds__(256) k_fft_axis(const void* __restrict__ in, i
       }
       if (ss.lam_off[ss.d - 1] >= 0) den += lam[ss.lam_off[ss.d - 1] + k];
       const T inv = (T)(1.0 / den);
-      cpx<T> v = buf[l * ls + k * ks];
+      const cpx<T> v = buf[l * ls + k * ks];
       buf[l * ls + k * ks] = {v.re * inv, v.im * inv};
     }
     __syncthreads();
-    smem_lines_fft<T>(buf, tmp, L, n, ls, ks, tw, true, pow2, bits);
+    lines_fft<T>(buf, tmp, L, n, ls, ks, ts, true, lo_lines);
   }
-  for (int e = threadIdx.x; e < L * n; e += blockDim.x) {
-    int l, k;
-    if (lo_lines) { l = e % L; k = e / L; } else { l = e / n; k = e % n; }
-    const int64_t lo = lo_lines ? lo0 + l : 0;
-    const int64_t hh = lo_lines ? hi0 : hi0 + l;
-    if (lo < st && hh < hi) {
-      const int64_t g = lo + st * (k + (int64_t)n * hh);
+  // ---- store ----
+  if (mode == FFT_R2C) {
+    // X[k] = E[k] + w^k O[k], k = 0..h, with E = (Z[k] + conj Z[h-k]) / 2,
+    // O = -i (Z[k] - conj Z[h-k]) / 2, Z[h] = Z[0]
+    for (int e = threadIdx.x; e < L * (hn + 1); e += blockDim.x) {
+      const int l = e / (hn + 1), k = e % (hn + 1);
+      const int64_t line = hi0 + l;
+      if (line >= hi) continue;
+      const cpx<T> a = buf[l * ls + (k % nt) * ks];
+      const cpx<T> b = cconjt(buf[l * ls + ((nt - k) % nt) * ks]);
+      const cpx<T> E = {(a.re + b.re) * T(0.5), (a.im + b.im) * T(0.5)};
+      const cpx<T> D = {(a.re - b.re) * T(0.5), (a.im - b.im) * T(0.5)};
+      const cpx<T> O = {D.im, -D.re};  // -i D
+      const cpx<T> wO = cmulc(tw[k % n], O);
+      reinterpret_cast<cpx<T>*>(out)[line * (hn + 1) + k] = cadd(E, wO);
+    }
+  } else if (mode == FFT_C2R) {
+    for (int e = threadIdx.x; e < L * nt; e += blockDim.x) {
+      const int l = e / nt, k = e % nt;
+      const int64_t line = hi0 + l;
+      if (line >= hi) continue;
       const cpx<T> v = buf[l * ls + k * ks];
-      if (out_real) reinterpret_cast<T*>(out)[g] = (T)(v.re * out_scale);
-      else reinterpret_cast<cpx<T>*>(out)[g] = v;
+      T* x = reinterpret_cast<T*>(out) + line * n;
+      x[2 * k] = (T)(v.re * out_scale);
+      x[2 * k + 1] = (T)(v.im * out_scale);
+    }
+  } else {
+    for (int e = threadIdx.x; e < L * n; e += blockDim.x) {
+      int l, k;
+      if (lo_lines) { l = e % L; k = e / L; } else { l = e / n; k = e % n; }
+      const int64_t lo = lo_lines ? lo0 + l : 0;
+      const int64_t hh = lo_lines ? hi0 : hi0 + l;
+      if (lo < st && hh < hi) {
+        const cpx<T> v = buf[l * ls + k * ks];
+        if (out_scale != 1.0) {
+          reinterpret_cast<cpx<T>*>(out)[lo + st * (k + (int64_t)n * hh)] =
+              {(T)(v.re * out_scale), (T)(v.im * out_scale)};
+        } else {
+          reinterpret_cast<cpx<T>*>(out)[lo + st * (k + (int64_t)n * hh)] = v;
+        }
+      }
     }
   }
+}
+
+__device__ __forceinline__ void cpa8(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cpa_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// Persistent, double-buffered variant for power-of-two transform lengths:
+// while tile t is transformed in one buffer, tile t+1 streams into the other
+// (cp.async), so HBM stays busy through the butterflies.  Same modes and
+// semantics as k_fft_axis.  Tile = L lines; `ntiles` tiles in total.
+template <typename T>
+__global__ void __launch_bounds__(256) k_fft_axis_p(const void* __restrict__ in, void* __restrict__ out,
+                                                    int mode, double out_scale, int64_t st, int n,
+                                                    int64_t hi, int L, int64_t ntiles,
+                                                    const cpx<T>* __restrict__ tw, int inverse,
+                                                    SolveSpec ss, const double* __restrict__ lam) {
+  extern __shared__ __align__(16) unsigned char fft_smem[];
+  const int nt = (mode == FFT_C2C) ? n : n / 2;
+  const int hn = n / 2;
+  const int bufc = L * (nt + 1);  // complex slots per buffer (C2R stages hn+1 per line)
+  cpx<T>* ts = reinterpret_cast<cpx<T>*>(fft_smem);
+  cpx<T>* bufs[2] = {ts + nt, ts + nt + bufc};
+  for (int m = threadIdx.x; m < nt; m += blockDim.x) ts[m] = tw[(mode == FFT_C2C) ? m : 2 * m];
+  const bool lo_lines = st > 1;
+  const int64_t nlob = lo_lines ? (st + L - 1) / L : 1;
+  const int64_t ls = lo_lines ? 1 : nt, ks = lo_lines ? L : 1;
+  auto tile_origin = [&](int64_t t, int64_t& lo0, int64_t& hi0) {
+    if (!lo_lines) {
+      lo0 = 0;
+      hi0 = t * L;
+    } else {
+      lo0 = (t % nlob) * L;
+      hi0 = t / nlob;
+    }
+  };
+  // async copy of tile t's input into buffer b
+  auto load = [&](int64_t t, int b) {
+    if (t < ntiles) {
+      int64_t lo0, hi0;
+      tile_origin(t, lo0, hi0);
+      cpx<T>* buf = bufs[b];
+      const uint32_t sb = (uint32_t)__cvta_generic_to_shared(buf);
+      if (mode == FFT_R2C) {
+        // L contiguous real lines of n = L * nt complex-sized slots, verbatim
+        const int64_t lines = (hi - hi0) < L ? (hi - hi0) : L;
+        const T* src = reinterpret_cast<const T*>(in) + hi0 * n;
+        const int64_t bytes = lines * n * (int64_t)sizeof(T);
+        for (int64_t o = threadIdx.x * 16; o < bytes; o += blockDim.x * 16)
+          cpa16(sb + (uint32_t)o, reinterpret_cast<const unsigned char*>(src) + o);
+      } else if (mode == FFT_C2R) {
+        // L contiguous lines of hn+1 complex, staged as [l][hn+1]
+        const int64_t lines = (hi - hi0) < L ? (hi - hi0) : L;
+        const cpx<T>* src = reinterpret_cast<const cpx<T>*>(in) + hi0 * (hn + 1);
+        for (int64_t e = threadIdx.x; e < lines * (hn + 1); e += blockDim.x) {
+          if (sizeof(cpx<T>) == 8) cpa8(sb + (uint32_t)(e * sizeof(cpx<T>)), src + e);
+          else cpa16(sb + (uint32_t)(e * sizeof(cpx<T>)), src + e);
+        }
+      } else {
+        const cpx<T>* src = reinterpret_cast<const cpx<T>*>(in);
+        for (int e = threadIdx.x; e < L * nt; e += blockDim.x) {
+          int l, k;
+          if (lo_lines) { l = e % L; k = e / L; } else { l = e / nt; k = e % nt; }
+          const int64_t lo = lo_lines ? lo0 + l : 0;
+          const int64_t hh = lo_lines ? hi0 : hi0 + l;
+          if (lo < st && hh < hi) {
+            const uint32_t d = sb + (uint32_t)((l * ls + k * ks) * sizeof(cpx<T>));
+            const cpx<T>* s = src + lo + st * (k + (int64_t)n * hh);
+            if (sizeof(cpx<T>) == 8) cpa8(d, s);
+            else cpa16(d, s);
+          }
+        }
+      }
+    }
+    cpa_commit();
+  };
+  int64_t t = blockIdx.x;
+  load(t, 0);
+  int b = 0;
+  for (; t < ntiles; t += gridDim.x, b ^= 1) {
+    load(t + gridDim.x, b ^ 1);
+    cpa_wait1();
+    __syncthreads();
+    cpx<T>* buf = bufs[b];
+    int64_t lo0, hi0;
+    tile_origin(t, lo0, hi0);
+    if (mode == FFT_C2R) {
+      // staged X[l][0..hn] -> Z[l][k] = E + i O in place (Z needs X[k], X[hn-k])
+      cpx<T> zv[8];
+      int cnt = 0;
+      for (int e = threadIdx.x; e < L * nt && cnt < 8; e += blockDim.x, ++cnt) {
+        const int l = e / nt, k = e % nt;
+        const cpx<T> a = buf[l * (hn + 1) + k], bb = cconjt(buf[l * (hn + 1) + hn - k]);
+        const cpx<T> E = {(a.re + bb.re) * T(0.5), (a.im + bb.im) * T(0.5)};
+        cpx<T> w = tw[k];
+        w.im = -w.im;
+        const cpx<T> D = {(a.re - bb.re) * T(0.5), (a.im - bb.im) * T(0.5)};
+        const cpx<T> O = cmulc(D, w);
+        zv[cnt] = {E.re - O.im, E.im + O.re};
+      }
+      __syncthreads();
+      cnt = 0;
+      for (int e = threadIdx.x; e < L * nt && cnt < 8; e += blockDim.x, ++cnt) buf[e] = zv[cnt];
+      __syncthreads();
+    }
+    stockham_lines<T, 4>(buf, L, nt, ls, ks, ts, (mode == FFT_C2R) || inverse != 0, lo_lines);
+    if (ss.active) {
+      for (int e = threadIdx.x; e < L * n; e += blockDim.x) {
+        int l, k;
+        if (lo_lines) { l = e % L; k = e / L; } else { l = e / n; k = e % n; }
+        const int64_t lo = lo_lines ? lo0 + l : 0;
+        double den = 1.0;
+        int64_t rem = lo;
+        for (int a = 0; a < ss.d - 1; ++a) {
+          const int64_t j = rem % ss.dims[a];
+          rem /= ss.dims[a];
+          if (ss.lam_off[a] >= 0) den += lam[ss.lam_off[a] + j];
+        }
+        if (ss.lam_off[ss.d - 1] >= 0) den += lam[ss.lam_off[ss.d - 1] + k];
+        const T inv = (T)(1.0 / den);
+        const cpx<T> v = buf[l * ls + k * ks];
+        buf[l * ls + k * ks] = {v.re * inv, v.im * inv};
+      }
+      __syncthreads();
+      stockham_lines<T, 4>(buf, L, n, ls, ks, ts, true, lo_lines);
+    }
+    // ---- store ----
+    if (mode == FFT_R2C) {
+      for (int e = threadIdx.x; e < L * (hn + 1); e += blockDim.x) {
+        const int l = e / (hn + 1), k = e % (hn + 1);
+        const int64_t line = hi0 + l;
+        if (line >= hi) continue;
+        const cpx<T> a = buf[l * ls + (k % nt) * ks];
+        const cpx<T> bb = cconjt(buf[l * ls + ((nt - k) % nt) * ks]);
+        const cpx<T> E = {(a.re + bb.re) * T(0.5), (a.im + bb.im) * T(0.5)};
+        const cpx<T> D = {(a.re - bb.re) * T(0.5), (a.im - bb.im) * T(0.5)};
+        const cpx<T> O = {D.im, -D.re};
+        const cpx<T> wO = cmulc(tw[k % n], O);
+        reinterpret_cast<cpx<T>*>(out)[line * (hn + 1) + k] = cadd(E, wO);
+      }
+    } else if (mode == FFT_C2R) {
+      for (int e = threadIdx.x; e < L * nt; e += blockDim.x) {
+        const int l = e / nt, k = e % nt;
+        const int64_t line = hi0 + l;
+        if (line >= hi) continue;
+        const cpx<T> v = buf[l * ls + k * ks];
+        T* x = reinterpret_cast<T*>(out) + line * n;
+        x[2 * k] = (T)(v.re * out_scale);
+        x[2 * k + 1] = (T)(v.im * out_scale);
+      }
+    } else {
+      for (int e = threadIdx.x; e < L * n; e += blockDim.x) {
+        int l, k;
+        if (lo_lines) { l = e % L; k = e / L; } else { l = e / n; k = e % n; }
+        const int64_t lo = lo_lines ? lo0 + l : 0;
+        const int64_t hh = lo_lines ? hi0 : hi0 + l;
+        if (lo < st && hh < hi) {
+          cpx<T> v = buf[l * ls + k * ks];
+          if (out_scale != 1.0) v = {(T)(v.re * out_scale), (T)(v.im * out_scale)};
+          reinterpret_cast<cpx<T>*>(out)[lo + st * (k + (int64_t)n * hh)] = v;
+        }
+      }
+    }
+    __syncthreads();  // buffer b is reloaded two iterations later
+  }
+}
+
+// Power-of-two persistent pass (L, nt powers of two; host checks).  Same
+// semantics as k_fft_axis; double-buffered cp.async tiles, shift indexing,
+// per-line solve denominators.
+template <typename T>
+__global__ void __launch_bounds__(256) k_fft_p2(const void* __restrict__ in, void* __restrict__ out,
+                                                int mode, double out_scale, int64_t st, int n,
+                                                int64_t hi, int lL, int64_t ntiles,
+                                                const cpx<T>* __restrict__ tw, int inverse,
+                                                SolveSpec ss, const double* __restrict__ lam) {
+  extern __shared__ __align__(16) unsigned char fft_smem[];
+  const int nt = (mode == FFT_C2C) ? n : n / 2;
+  int ln = 0;
+  while ((1 << ln) < nt) ++ln;
+  const int L = 1 << lL;
+  const int hn = n / 2;
+  const int bufc = L * (nt + 1);
+  cpx<T>* ts = reinterpret_cast<cpx<T>*>(fft_smem);
+  cpx<T>* bufs[2] = {ts + nt, ts + nt + bufc};
+  __shared__ double denl[16];
+  for (int m = threadIdx.x; m < nt; m += blockDim.x) ts[m] = tw[(mode == FFT_C2C) ? m : 2 * m];
+  const bool lo_lines = st > 1;
+  const int64_t nlob = lo_lines ? (st + L - 1) >> lL : 1;
+  auto origin = [&](int64_t t, int64_t& lo0, int64_t& hi0) {
+    if (!lo_lines) {
+      lo0 = 0;
+      hi0 = t << lL;
+    } else {
+      lo0 = (t % nlob) << lL;
+      hi0 = t / nlob;
+    }
+  };
+  auto sidx = [&](int l, int k) -> int { return lo_lines ? (k << lL) + l : (l << ln) + k; };
+  auto load = [&](int64_t t, int b) {
+    if (t < ntiles) {
+      int64_t lo0, hi0;
+      origin(t, lo0, hi0);
+      const uint32_t sb = (uint32_t)__cvta_generic_to_shared(bufs[b]);
+      if (mode == FFT_R2C) {
+        const int64_t lines = (hi - hi0) < L ? (hi - hi0) : L;
+        const unsigned char* src = reinterpret_cast<const unsigned char*>(in) + hi0 * n * (int64_t)sizeof(T);
+        const int64_t bytes = lines * n * (int64_t)sizeof(T);
+        for (int64_t o = threadIdx.x * 16; o < bytes; o += blockDim.x * 16) cpa16(sb + (uint32_t)o, src + o);
+      } else if (mode == FFT_C2R) {
+        const int64_t lines = (hi - hi0) < L ? (hi - hi0) : L;
+        const cpx<T>* src = reinterpret_cast<const cpx<T>*>(in) + hi0 * (hn + 1);
+        const int64_t cnt = lines * (hn + 1);
+        for (int64_t e = threadIdx.x; e < cnt; e += blockDim.x) {
+          if (sizeof(cpx<T>) == 8) cpa8(sb + (uint32_t)(e * 8), src + e);
+          else cpa16(sb + (uint32_t)(e * 16), src + e);
+        }
+      } else {
+        const cpx<T>* src = reinterpret_cast<const cpx<T>*>(in);
+        const int tot = L << ln;
+        for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+          const int l = lo_lines ? (e & (L - 1)) : (e >> ln);
+          const int k = lo_lines ? (e >> lL) : (e & (nt - 1));
+          const int64_t lo = lo_lines ? lo0 + l : 0;
+          const int64_t hh = lo_lines ? hi0 : hi0 + l;
+          if (lo < st && hh < hi) {
+            const uint32_t d = sb + (uint32_t)(sidx(l, k) * (int)sizeof(cpx<T>));
+            const cpx<T>* s = src + lo + st * (k + (int64_t)n * hh);
+            if (sizeof(cpx<T>) == 8) cpa8(d, s);
+            else cpa16(d, s);
+          }
+        }
+      }
+    }
+    cpa_commit();
+  };
+  int64_t t = blockIdx.x;
+  load(t, 0);
+  int b = 0;
+  for (; t < ntiles; t += gridDim.x, b ^= 1) {
+    load(t + gridDim.x, b ^ 1);
+    cpa_wait1();
+    int64_t lo0, hi0;
+    origin(t, lo0, hi0);
+    if (ss.active && threadIdx.x < L) {
+      // per-line part of the denominator: axes 0..d-2 from the line's lo index
+      double den = 1.0;
+      int64_t rem = lo0 + threadIdx.x;
+      for (int a = 0; a < ss.d - 1; ++a) {
+        const int64_t j = rem % ss.dims[a];
+        rem /= ss.dims[a];
+        if (ss.lam_off[a] >= 0) den += lam[ss.lam_off[a] + j];
+      }
+      denl[threadIdx.x] = den;
+    }
+    __syncthreads();
+    cpx<T>* buf = bufs[b];
+    if (mode == FFT_C2R) {
+      // staged X[l][0..hn] -> Z[l][k] = E + i O (registers, then in place)
+      cpx<T> zv[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int e = threadIdx.x + c * blockDim.x;
+        if (e < (L << ln)) {
+          const int l = e >> ln, k = e & (nt - 1);
+          const cpx<T> a = buf[l * (hn + 1) + k], bb = cconjt(buf[l * (hn + 1) + hn - k]);
+          const cpx<T> E = {(a.re + bb.re) * T(0.5), (a.im + bb.im) * T(0.5)};
+          cpx<T> w = tw[k];
+          w.im = -w.im;
+          const cpx<T> D = {(a.re - bb.re) * T(0.5), (a.im - bb.im) * T(0.5)};
+          const cpx<T> O = cmulc(D, w);
+          zv[c] = {E.re - O.im, E.im + O.re};
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int e = threadIdx.x + c * blockDim.x;
+        if (e < (L << ln)) buf[e] = zv[c];
+      }
+      __syncthreads();
+    }
+    stockham_p2<T, 4>(buf, lL, ln, ts, (mode == FFT_C2R) || inverse != 0, lo_lines);
+    if (ss.active) {
+      const int tot = L << ln;
+      const int lo_off = ss.lam_off[ss.d - 1];
+      for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+        const int l = lo_lines ? (e & (L - 1)) : (e >> ln);
+        const int k = lo_lines ? (e >> lL) : (e & (nt - 1));
+        const double den = denl[l] + (lo_off >= 0 ? lam[lo_off + k] : 0.0);
+        const T inv = (T)(1.0 / den);
+        const cpx<T> v = buf[e];
+        buf[e] = {v.re * inv, v.im * inv};
+      }
+      __syncthreads();
+      stockham_p2<T, 4>(buf, lL, ln, ts, true, lo_lines);
+    }
+    // ---- store ----
+    if (mode == FFT_R2C) {
+      for (int l = 0; l < L; ++l) {
+        const int64_t line = hi0 + l;
+        if (line >= hi) break;
+        cpx<T>* dst = reinterpret_cast<cpx<T>*>(out) + line * (hn + 1);
+        for (int k = threadIdx.x; k <= hn; k += blockDim.x) {
+          const cpx<T> a = buf[(l << ln) + (k & (nt - 1))];
+          const cpx<T> bb = cconjt(buf[(l << ln) + ((nt - k) & (nt - 1))]);
+          const cpx<T> E = {(a.re + bb.re) * T(0.5), (a.im + bb.im) * T(0.5)};
+          const cpx<T> D = {(a.re - bb.re) * T(0.5), (a.im - bb.im) * T(0.5)};
+          const cpx<T> O = {D.im, -D.re};
+          dst[k] = cadd(E, cmulc(tw[k], O));
+        }
+      }
+    } else if (mode == FFT_C2R) {
+      const int tot = L << ln;
+      for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+        const int l = e >> ln, k = e & (nt - 1);
+        const int64_t line = hi0 + l;
+        if (line >= hi) continue;
+        const cpx<T> v = buf[e];
+        T* x = reinterpret_cast<T*>(out) + line * n;
+        x[2 * k] = (T)(v.re * out_scale);
+        x[2 * k + 1] = (T)(v.im * out_scale);
+      }
+    } else {
+      const int tot = L << ln;
+      for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+        const int l = lo_lines ? (e & (L - 1)) : (e >> ln);
+        const int k = lo_lines ? (e >> lL) : (e & (nt - 1));
+        const int64_t lo = lo_lines ? lo0 + l : 0;
+        const int64_t hh = lo_lines ? hi0 : hi0 + l;
+        if (lo < st && hh < hi) {
+          cpx<T> v = buf[e];
+          if (out_scale != 1.0) v = {(T)(v.re * out_scale), (T)(v.im * out_scale)};
+          reinterpret_cast<cpx<T>*>(out)[lo + st * (k + (int64_t)n * hh)] = v;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// real <-> complex conversion for the full-spectrum fallback (odd n0)
+template <typename T>
+__global__ void k_real_to_cpx(const T* __restrict__ x, cpx<T>* __restrict__ z, int64_t N) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += stride)
+    z[i] = {x[i], T(0)};
+}
+template <typename T>
+__global__ void k_cpx_to_real(const cpx<T>* __restrict__ z, T* __restrict__ x, int64_t N,
+                              double scale) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += stride)
+    x[i] = (T)(z[i].re * scale);
 }
 
 // 4 sin^2(pi j / n) for j < n

@@ -680,6 +680,13 @@ int tr_admm_read(void* handle, int which, void* dst, void* stream) {
   return rd((Solver<double>*)h->solver);
 }
 
+void* tr_admm_stream(void* handle) {
+  if (!handle) return nullptr;
+  auto* h = (AdmmHandle*)handle;
+  if (h->dtype == TR_F32) return (void*)((Solver<float>*)h->solver)->streams[0];
+  return (void*)((Solver<double>*)h->solver)->streams[0];
+}
+
 int tr_admm_destroy(void* handle) {
   if (!handle) return 0;
   auto* h = (AdmmHandle*)handle;
