@@ -134,7 +134,7 @@ static int fft_solve(Solver<T>& s, const T* rhs, T* out, cudaStream_t st) {
       const int64_t grid = std::min<int64_t>(ntiles, 2 * (int64_t)num_sms());
       const size_t smem = ((size_t)nt + 2 * (size_t)L * (nt + 1)) * sizeof(cpx<T>);
       launch("fft", k_fft_p2<T>, (unsigned)grid, 256, smem, st, in, dst, mode, scale, stv, n, hi,
-             lL, ntiles, (const cpx<T>*)s.tw[a], inverse, ss, (const double*)s.lam);
+             lL, ntiles, (const cpx<T>*)s.tw[a], inverse, ss, (const double*)s.lam, (int64_t)0);
       return 0;
     }
     // at most 4096 complex line elements per CTA (8 radix-2 groups per thread)
@@ -173,6 +173,114 @@ static int fft_solve(Solver<T>& s, const T* rhs, T* out, cudaStream_t st) {
     launch("fft", k_cpx_to_real<T>, eg, kRedThreads, 0, st, (const cpx<T>*)s.spec, out, g.N,
            1.0 / (double)g.N);
   }
+  TR_LAUNCH_CHECK();
+  return 0;
+}
+
+// One C2C pass along a spectrum axis of length n (lo-stride stv, hi lines of
+// lines); persistent power-of-two kernel when possible, generic otherwise.
+template <typename T>
+static int fft_c2c(const cpx<T>* tw, const double* lam, void* data, int n, int64_t stv, int64_t hi,
+                   int inverse, const SolveSpec& ss, cudaStream_t st) {
+  const bool pow2 = (n & (n - 1)) == 0;
+  if (pow2 && n >= 8 && n <= 2048 && getenv("TR_FFT_SIMPLE") == nullptr) {
+    static bool pattr = false;
+    if (!pattr) {
+      cudaFuncSetAttribute(k_fft_p2<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      pattr = true;
+    }
+    const int64_t cap = std::min<int64_t>(std::min<int64_t>(16, 2048 / n), stv == 1 ? hi : stv);
+    int lL = 0;
+    while ((2ll << lL) <= cap) ++lL;
+    const int64_t L = 1ll << lL;
+    const int64_t ntiles = stv == 1 ? cdiv(hi, L) : hi * cdiv(stv, L);
+    const int64_t grid = std::min<int64_t>(ntiles, 2 * (int64_t)num_sms());
+    const size_t smem = ((size_t)n + 2 * (size_t)L * (n + 1)) * sizeof(cpx<T>);
+    launch("fft", k_fft_p2<T>, (unsigned)grid, 256, smem, st, (const void*)data, data,
+           (int)FFT_C2C, 1.0, stv, n, hi, lL, ntiles, tw, inverse, ss, lam, (int64_t)0);
+    return 0;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_fft_axis<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  int64_t L = std::max<int64_t>(1, std::min<int64_t>(16, 4096 / n));
+  L = std::min<int64_t>(L, stv == 1 ? hi : stv);
+  TR_REQUIRE(n <= 4096, "FFT axis of length %d exceeds the 4096-point tile", n);
+  const int64_t grid = stv == 1 ? cdiv(hi, L) : hi * cdiv(stv, L);
+  const size_t smem = ((size_t)n + (size_t)L * n * (pow2 ? 1 : 2)) * sizeof(cpx<T>);
+  launch("fft", k_fft_axis<T>, (unsigned)grid, 256, smem, st, (const void*)data, data,
+         (int)FFT_C2C, 1.0, stv, n, hi, (int)L, tw, inverse, ss, lam);
+  return 0;
+}
+
+// FFT solve with the half spectrum stored axes-(1, 0)-swapped: every pass
+// streams >= 32-byte segments and the axis-1 pass runs on contiguous lines.
+// Falls back to fft_solve when axis 0 is not an even power-of-two length.
+template <typename T>
+static int fft_solve2(Solver<T>& s, const T* rhs, T* out, cudaStream_t st) {
+  const Geom& g = s.g;
+  const int d = g.d;
+  const int64_t n0 = g.dims[0], n1 = g.dims[1];
+  const int hn = (int)(n0 / 2);
+  const bool ok = n0 % 2 == 0 && (hn & (hn - 1)) == 0 && hn >= 8 && hn <= 2048 &&
+                  (n0 * (int64_t)sizeof(T)) % 16 == 0 && getenv("TR_FFT_SIMPLE") == nullptr;
+  if (!ok) return fft_solve<T>(s, rhs, out, st);
+  int64_t sd[kMaxOrder], sst[kMaxOrder];
+  int orig[kMaxOrder];
+  sd[0] = n1;
+  orig[0] = 1;
+  sd[1] = hn + 1;
+  orig[1] = 0;
+  for (int a = 2; a < d; ++a) {
+    sd[a] = g.dims[a];
+    orig[a] = a;
+  }
+  int64_t SN = 1;
+  for (int a = 0; a < d; ++a) {
+    sst[a] = SN;
+    SN *= sd[a];
+  }
+  SolveSpec off = s.ss, on = s.ss;
+  off.active = 0;
+  on.active = 1;
+  for (int p = 0; p < d; ++p) {
+    off.dims[p] = on.dims[p] = sd[p];
+    off.lam_off[p] = on.lam_off[p] = s.ss.lam_off[orig[p]];
+  }
+  const cpx<T>* const* tw = (const cpx<T>* const*)s.tw.data();
+  static bool pattr = false;
+  if (!pattr) {
+    cudaFuncSetAttribute(k_fft_p2<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    pattr = true;
+  }
+  // axis 0, real -> half spectrum (swapped layout)
+  const int64_t lines = g.N / n0;
+  auto r2c_like = [&](int mode, const void* in, void* dst, double scale) {
+    const int64_t cap = std::min<int64_t>(std::min<int64_t>(16, 2048 / hn), lines);
+    int lL = 0;
+    while ((2ll << lL) <= cap) ++lL;
+    const int64_t L = 1ll << lL;
+    const int64_t ntiles = cdiv(lines, L);
+    const int64_t grid = std::min<int64_t>(ntiles, 2 * (int64_t)num_sms());
+    const size_t smem = ((size_t)hn + 2 * (size_t)L * (hn + 1)) * sizeof(cpx<T>);
+    launch("fft", k_fft_p2<T>, (unsigned)grid, 256, smem, st, in, dst, mode, scale, (int64_t)1,
+           (int)n0, lines, lL, ntiles, tw[0], 0, off, (const double*)s.lam, n1);
+  };
+  r2c_like(FFT_R2C, rhs, s.spec, 1.0);
+  for (int p = 0; p < d - 1; ++p) {
+    if (p == 1) continue;  // spectral position 1 is axis 0, already transformed
+    if (fft_c2c<T>(tw[orig[p]], s.lam, s.spec, (int)sd[p], sst[p], SN / (sst[p] * sd[p]), 0, off, st))
+      return 1;
+  }
+  if (fft_c2c<T>(tw[orig[d - 1]], s.lam, s.spec, (int)sd[d - 1], sst[d - 1], 1, 0, on, st)) return 1;
+  for (int p = d - 2; p >= 0; --p) {
+    if (p == 1) continue;
+    if (fft_c2c<T>(tw[orig[p]], s.lam, s.spec, (int)sd[p], sst[p], SN / (sst[p] * sd[p]), 1, off, st))
+      return 1;
+  }
+  r2c_like(FFT_C2R, s.spec, out, 2.0 / (double)g.N);
   TR_LAUNCH_CHECK();
   return 0;
 }
@@ -252,7 +360,7 @@ static int admm_step(Solver<T>& s, double* hout) {
     } else {
       launch("admm_rhs", k_admm_rhs<T>, grid, kRedThreads, 0, st, g, s.A, s.e, s.y, mu, gp, lp,
              s.rhs);
-      if (fft_solve<T>(s, s.rhs, s.l, st)) return 1;
+      if (fft_solve2<T>(s, s.rhs, s.l, st)) return 1;
     }
     tau = 1.0 / (gamma * mu);
     for (int k = 0; k < nm; ++k)
@@ -313,7 +421,7 @@ static int admm_step(Solver<T>& s, double* hout) {
     } else {
       launch("admm_rhs", k_admm_rhs<T>, grid, kRedThreads, 0, st, g, (const T*)s.l, (const T*)nullptr,
              s.y, mu, gp, lp, s.rhs);
-      if (fft_solve<T>(s, s.rhs, s.z, st)) return 1;
+      if (fft_solve2<T>(s, s.rhs, s.z, st)) return 1;
     }
     tau = s.cfg.lam / (gamma * mu);
     for (int k = 0; k < nm; ++k)

@@ -21,7 +21,7 @@
 namespace tr {
 
 template <typename T>
-struct cpx {
+struct __align__(2 * sizeof(T)) cpx {
   T re, im;
 };
 
@@ -123,16 +123,36 @@ __device__ void stockham_lines(cpx<T>* buf, int L, int n, int64_t ls, int64_t ks
 // ln = log2 n) with 32-bit shared-memory indices: no integer division in the
 // butterfly loops.  Layout: lo_major -> element (l, k) at (k << lL) + l,
 // otherwise (l << ln) + k.
+// Per-stage twiddle tables for the radix-4/2 Stockham sequence of an n-point
+// transform: stage (Ns, R) holds w^{jm r n/(Ns R)} at jm*(R-1) + r-1, so a
+// warp's twiddle reads are consecutive (stride R-1) instead of all hitting one
+// bank.  Total size < n.  `full` = exp(-2 pi i m / n) table (global).
+template <typename T>
+__device__ void build_stage_twiddles(cpx<T>* st_tab, int ln, const cpx<T>* full, int full_step) {
+  int lNs = 0, off = 0;
+  while (lNs < ln) {
+    const int lR = (ln - lNs) >= 2 ? 2 : 1;
+    const int R = 1 << lR, Ns = 1 << lNs;
+    const int tws = ln - lNs - lR;
+    for (int e = threadIdx.x; e < Ns * (R - 1); e += blockDim.x) {
+      const int jm = e / (R - 1), r = e % (R - 1) + 1;
+      st_tab[off + e] = full[((jm * r) << tws) * full_step];
+    }
+    off += Ns * (R - 1);
+    lNs += lR;
+  }
+}
+
 template <typename T, int GMAX>
-__device__ void stockham_p2(cpx<T>* buf, int lL, int ln, const cpx<T>* ts, bool inverse,
+__device__ void stockham_p2(cpx<T>* buf, int lL, int ln, const cpx<T>* st_tab, bool inverse,
                             bool lo_major) {
   const int n = 1 << ln;
-  int lNs = 0;
+  int lNs = 0, toff = 0;
   while (lNs < ln) {
     const int lR = (ln - lNs) >= 2 ? 2 : 1;
     const int lg = ln - lR;  // log2(groups)
     const int total = 1 << (lL + lg);
-    const int tws = ln - lNs - lR;  // log2(n / (Ns R))
+    const int rm1 = (1 << lR) - 1;
     const int nsm = (1 << lNs) - 1;
     cpx<T> v[GMAX][4];
 #pragma unroll
@@ -148,7 +168,7 @@ __device__ void stockham_p2(cpx<T>* buf, int lL, int ln, const cpx<T>* ts, bool 
             const int k = j + (r << lg);
             cpx<T> x = buf[lo_major ? (k << lL) + l : (l << ln) + k];
             if (r > 0 && jm > 0) {
-              cpx<T> w = ts[(jm * r) << tws];
+              cpx<T> w = st_tab[toff + jm * rm1 + r - 1];
               if (inverse) w.im = -w.im;
               x = cmulc(x, w);
             }
@@ -185,6 +205,7 @@ __device__ void stockham_p2(cpx<T>* buf, int lL, int ln, const cpx<T>* ts, bool 
       }
     }
     __syncthreads();
+    toff += (1 << lNs) * rm1;
     lNs += lR;
   }
   (void)n;
@@ -238,7 +259,7 @@ enum FftMode { FFT_C2C = 0, FFT_R2C = 1, FFT_C2R = 2 };
 //  C2R (axis 0 only): inverse of R2C, real output times out_scale.
 // `ss.active` (C2C on the last axis): forward, divide, inverse.
 template <typename T>
-__global__ void __launch_bounds__(256) k_fft_axis(const void* __restrict__ in, void* __restrict__ out,
+__global__ void __launch_bounds__(256) k_fft_axis(const void* in, void* out,  // may alias (in-place passes)
                                                   int mode, double out_scale, int64_t st, int n,
                                                   int64_t hi, int L,
                                                   const cpx<T>* __restrict__ tw, int inverse,
@@ -386,7 +407,7 @@ __device__ __forceinline__ void cpa_wait1() { asm volatile("cp.async.wait_group 
 // (cp.async), so HBM stays busy through the butterflies.  Same modes and
 // semantics as k_fft_axis.  Tile = L lines; `ntiles` tiles in total.
 template <typename T>
-__global__ void __launch_bounds__(256) k_fft_axis_p(const void* __restrict__ in, void* __restrict__ out,
+__global__ void __launch_bounds__(256) k_fft_axis_p(const void* in, void* out,  // may alias (in-place passes)
                                                     int mode, double out_scale, int64_t st, int n,
                                                     int64_t hi, int L, int64_t ntiles,
                                                     const cpx<T>* __restrict__ tw, int inverse,
@@ -544,12 +565,16 @@ __global__ void __launch_bounds__(256) k_fft_axis_p(const void* __restrict__ in,
 // Power-of-two persistent pass (L, nt powers of two; host checks).  Same
 // semantics as k_fft_axis; double-buffered cp.async tiles, shift indexing,
 // per-line solve denominators.
+// tr_n1 > 0 (R2C / C2R only): the half spectrum is stored with axes 0 and 1
+// swapped, bin k of line (i1, rest) at i1 + n1 * (k + (n/2+1) * rest), so the
+// axis-1 pass runs on contiguous lines.
 template <typename T>
-__global__ void __launch_bounds__(256) k_fft_p2(const void* __restrict__ in, void* __restrict__ out,
+__global__ void __launch_bounds__(256) k_fft_p2(const void* in, void* out,  // may alias (in-place passes)
                                                 int mode, double out_scale, int64_t st, int n,
                                                 int64_t hi, int lL, int64_t ntiles,
                                                 const cpx<T>* __restrict__ tw, int inverse,
-                                                SolveSpec ss, const double* __restrict__ lam) {
+                                                SolveSpec ss, const double* __restrict__ lam,
+                                                int64_t tr_n1) {
   extern __shared__ __align__(16) unsigned char fft_smem[];
   const int nt = (mode == FFT_C2C) ? n : n / 2;
   int ln = 0;
@@ -557,10 +582,11 @@ __global__ void __launch_bounds__(256) k_fft_p2(const void* __restrict__ in, voi
   const int L = 1 << lL;
   const int hn = n / 2;
   const int bufc = L * (nt + 1);
-  cpx<T>* ts = reinterpret_cast<cpx<T>*>(fft_smem);
-  cpx<T>* bufs[2] = {ts + nt, ts + nt + bufc};
+  cpx<T>* ts = reinterpret_cast<cpx<T>*>(fft_smem);  // per-stage twiddles (< nt entries)
+  cpx<T>* const buf0 = ts + nt;                       // two tile buffers of bufc slots
   __shared__ double denl[16];
-  for (int m = threadIdx.x; m < nt; m += blockDim.x) ts[m] = tw[(mode == FFT_C2C) ? m : 2 * m];
+  __shared__ int64_t lbase[16];  // R2C output base of each line of the tile
+  build_stage_twiddles<T>(ts, ln, tw, (mode == FFT_C2C) ? 1 : 2);
   const bool lo_lines = st > 1;
   const int64_t nlob = lo_lines ? (st + L - 1) >> lL : 1;
   auto origin = [&](int64_t t, int64_t& lo0, int64_t& hi0) {
@@ -577,19 +603,36 @@ __global__ void __launch_bounds__(256) k_fft_p2(const void* __restrict__ in, voi
     if (t < ntiles) {
       int64_t lo0, hi0;
       origin(t, lo0, hi0);
-      const uint32_t sb = (uint32_t)__cvta_generic_to_shared(bufs[b]);
+      const uint32_t sb = (uint32_t)__cvta_generic_to_shared(buf0 + b * bufc);
       if (mode == FFT_R2C) {
         const int64_t lines = (hi - hi0) < L ? (hi - hi0) : L;
         const unsigned char* src = reinterpret_cast<const unsigned char*>(in) + hi0 * n * (int64_t)sizeof(T);
         const int64_t bytes = lines * n * (int64_t)sizeof(T);
         for (int64_t o = threadIdx.x * 16; o < bytes; o += blockDim.x * 16) cpa16(sb + (uint32_t)o, src + o);
       } else if (mode == FFT_C2R) {
-        const int64_t lines = (hi - hi0) < L ? (hi - hi0) : L;
-        const cpx<T>* src = reinterpret_cast<const cpx<T>*>(in) + hi0 * (hn + 1);
-        const int64_t cnt = lines * (hn + 1);
-        for (int64_t e = threadIdx.x; e < cnt; e += blockDim.x) {
-          if (sizeof(cpx<T>) == 8) cpa8(sb + (uint32_t)(e * 8), src + e);
-          else cpa16(sb + (uint32_t)(e * 16), src + e);
+        const cpx<T>* X = reinterpret_cast<const cpx<T>*>(in);
+        const int cnt = L * (hn + 1);
+        if (tr_n1) {
+          // swapped layout: this thread always serves line l = tid mod L
+          const int l = threadIdx.x & (L - 1);
+          const int64_t line = hi0 + l;
+          if (line < hi) {
+            const int64_t gb = (line % tr_n1) + tr_n1 * (int64_t)(hn + 1) * (line / tr_n1);
+            for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+              const int k = e >> lL;
+              const uint32_t d = sb + (uint32_t)((l * (hn + 1) + k) * (int)sizeof(cpx<T>));
+              if (sizeof(cpx<T>) == 8) cpa8(d, X + gb + tr_n1 * k);
+              else cpa16(d, X + gb + tr_n1 * k);
+            }
+          }
+        } else {
+          for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+            const int l = e / (hn + 1), k = e % (hn + 1);
+            if (hi0 + l >= hi) continue;
+            const uint32_t d = sb + (uint32_t)(e * (int)sizeof(cpx<T>));
+            if (sizeof(cpx<T>) == 8) cpa8(d, X + (hi0 + l) * (hn + 1) + k);
+            else cpa16(d, X + (hi0 + l) * (hn + 1) + k);
+          }
         }
       } else {
         const cpx<T>* src = reinterpret_cast<const cpx<T>*>(in);
@@ -629,8 +672,13 @@ __global__ void __launch_bounds__(256) k_fft_p2(const void* __restrict__ in, voi
       }
       denl[threadIdx.x] = den;
     }
+    if (mode == FFT_R2C && threadIdx.x < L) {
+      const int64_t line = hi0 + threadIdx.x;
+      lbase[threadIdx.x] = tr_n1 ? (line % tr_n1) + tr_n1 * (int64_t)(hn + 1) * (line / tr_n1)
+                                 : line * (hn + 1);
+    }
     __syncthreads();
-    cpx<T>* buf = bufs[b];
+    cpx<T>* buf = buf0 + b * bufc;
     if (mode == FFT_C2R) {
       // staged X[l][0..hn] -> Z[l][k] = E + i O (registers, then in place)
       cpx<T> zv[8];
@@ -673,18 +721,21 @@ __global__ void __launch_bounds__(256) k_fft_p2(const void* __restrict__ in, voi
     }
     // ---- store ----
     if (mode == FFT_R2C) {
-      for (int l = 0; l < L; ++l) {
-        const int64_t line = hi0 + l;
-        if (line >= hi) break;
-        cpx<T>* dst = reinterpret_cast<cpx<T>*>(out) + line * (hn + 1);
-        for (int k = threadIdx.x; k <= hn; k += blockDim.x) {
-          const cpx<T> a = buf[(l << ln) + (k & (nt - 1))];
-          const cpx<T> bb = cconjt(buf[(l << ln) + ((nt - k) & (nt - 1))]);
-          const cpx<T> E = {(a.re + bb.re) * T(0.5), (a.im + bb.im) * T(0.5)};
-          const cpx<T> D = {(a.re - bb.re) * T(0.5), (a.im - bb.im) * T(0.5)};
-          const cpx<T> O = {D.im, -D.re};
-          dst[k] = cadd(E, cmulc(tw[k], O));
-        }
+      // element e -> (l, k); with the swapped layout l runs fastest so the L
+      // lines' bin k land in one contiguous segment
+      cpx<T>* Xo = reinterpret_cast<cpx<T>*>(out);
+      const int cnt = L * (hn + 1);
+      const int64_t kst = tr_n1 ? tr_n1 : 1;
+      for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+        const int l = tr_n1 ? (e & (L - 1)) : e / (hn + 1);
+        const int k = tr_n1 ? (e >> lL) : e % (hn + 1);
+        if (hi0 + l >= hi) continue;
+        const cpx<T> a = buf[(l << ln) + (k & (nt - 1))];
+        const cpx<T> bb = cconjt(buf[(l << ln) + ((nt - k) & (nt - 1))]);
+        const cpx<T> E = {(a.re + bb.re) * T(0.5), (a.im + bb.im) * T(0.5)};
+        const cpx<T> D = {(a.re - bb.re) * T(0.5), (a.im - bb.im) * T(0.5)};
+        const cpx<T> O = {D.im, -D.re};
+        Xo[lbase[l] + kst * k] = cadd(E, cmulc(tw[k], O));
       }
     } else if (mode == FFT_C2R) {
       const int tot = L << ln;
