@@ -165,9 +165,11 @@ def admm_bytes(shape, esize, nmodes=3):
     """Algorithmic HBM bytes per ADMM sweep of the non-LRTA kernels."""
     N = math.prod(shape)
     T = N * esize
-    cplx = 2 * T
     d = len(shape)
-    fft = (T + cplx) + (d - 2) * 2 * cplx + 2 * cplx + (d - 2) * 2 * cplx + (cplx + T)
+    # half spectrum along axis 0: (n0/2 + 1) / n0 of the complex volume
+    S = 2 * esize * (shape[0] // 2 + 1) * (N // shape[0])
+    # R2C (T in, S out), (d-2) forward + 1 solve + (d-2) inverse C2C passes, C2R (S in, T out)
+    fft = (T + S) + (d - 2) * 2 * S + 2 * S + (d - 2) * 2 * S + (S + T)
     return {
         "fft": fft,
         "admm_rhs": (3 + 2 * nmodes) * T + T,
@@ -256,7 +258,7 @@ def run_ours(args):
     # observations and mask, the sweeps, D2H of L and E, all inside the timer
     host = flat.reshape(tuple(reversed(dims))).permute(2, 1, 0).cpu().numpy()
     host_mask = np.ones(dims, dtype=bool)
-    e2e_iters = max(1, min(args.steps, 5))
+    e2e_iters = max(10, args.steps)
     if args.step == "admm":
         cfg_e2e = pk.SolverConfig(phi=pk.MCP(2.5), psi=pk.MCP(2.5), randomized=True, sketch=sk,
                                   max_iters=e2e_iters, tol=1e-30)
