@@ -495,6 +495,7 @@ static int admm_create(const AdmmConfig& cfg, int order, const int64_t* dims, co
   for (int i = 0; i < order; ++i) {
     g.dims[i] = dims[i];
     g.st[i] = g.N;
+    g.lst[i] = g.N / dims[0];
     g.N *= dims[i];
   }
   const int64_t N = g.N;

@@ -21,6 +21,7 @@ struct Geom {
   int d;
   int64_t dims[kMaxOrder];
   int64_t st[kMaxOrder];
+  int64_t lst[kMaxOrder];  // st[a] / dims[0]: stride of axis a in the line index
   int64_t N;
 };
 
@@ -33,9 +34,12 @@ __device__ __forceinline__ void axis_offsets(const Geom& g, int a, int64_t j, in
   next = j + 1 < n ? s : -s * (n - 1);
 }
 
-// coordinate of the line (index of axes 1..d-1 flattened) along axis a >= 1
+// coordinate of the line (index of axes 1..d-1 flattened) along axis a >= 1;
+// 32-bit division when the line count allows (it does for any tensor < 2^31 lines)
 __device__ __forceinline__ int64_t line_coord(const Geom& g, int64_t line, int a) {
-  const int64_t lst = g.st[a] / g.dims[0];
+  const int64_t lst = g.lst[a];
+  if (line < (1ll << 31) && lst < (1ll << 31) && g.dims[a] < (1ll << 31))
+    return (int64_t)(((uint32_t)line / (uint32_t)lst) % (uint32_t)g.dims[a]);
   return (line / lst) % g.dims[a];
 }
 
@@ -87,7 +91,7 @@ __global__ void __launch_bounds__(kRedThreads) k_admm_rhs(Geom g, const T* __res
                                                           ModePtrs<T> gm, ModePtrs<T> lag,
                                                           T* __restrict__ out) {
   const int64_t n0 = g.dims[0], lines = g.N / n0;
-  const T imu = T(1) / (T)mu;
+  const T imu = (T)(1.0 / mu);
   const bool pure = gm.count == 1 && gm.axis[0] < 0;
   for (int64_t line = blockIdx.x; line < lines; line += gridDim.x) {
     int64_t prevoff[kMaxOrder];
@@ -102,9 +106,9 @@ __global__ void __launch_bounds__(kRedThreads) k_admm_rhs(Geom g, const T* __res
     const int64_t base = line * n0;
     for (int64_t i0 = threadIdx.x; i0 < n0; i0 += blockDim.x) {
       const int64_t i = base + i0;
-      const T bv = (B ? (A[i] - B[i]) : A[i]) + y[i] / (T)mu;
+      const T bv = (B ? (A[i] - B[i]) : A[i]) + y[i] * imu;
       if (pure) {
-        out[i] = (T)0.5 * (bv + (gm.p[0][i] - lag.p[0][i] / (T)mu));
+        out[i] = (T)0.5 * (bv + (gm.p[0][i] - lag.p[0][i] * imu));
         continue;
       }
       T acc = bv;
@@ -113,8 +117,8 @@ __global__ void __launch_bounds__(kRedThreads) k_admm_rhs(Geom g, const T* __res
         if (k < gm.count) {
           const int a = gm.axis[k];
           const int64_t ip = a == 0 ? base + (i0 > 0 ? i0 - 1 : n0 - 1) : i + prevoff[k];
-          const T gi = gm.p[k][i] - lag.p[k][i] / (T)mu;
-          const T gp = gm.p[k][ip] - lag.p[k][ip] / (T)mu;
+          const T gi = gm.p[k][i] - lag.p[k][i] * imu;
+          const T gp = gm.p[k][ip] - lag.p[k][ip] * imu;
           acc += gp - gi;
         }
       }
@@ -129,6 +133,7 @@ template <typename T>
 __global__ void __launch_bounds__(kRedThreads) k_lrta_input(Geom g, const T* __restrict__ l,
                                                             int axis, const T* __restrict__ lag,
                                                             double mu, T* __restrict__ X) {
+  const T imu = (T)(1.0 / mu);
   const int64_t n0 = g.dims[0], lines = g.N / n0;
   for (int64_t line = blockIdx.x; line < lines; line += gridDim.x) {
     int64_t pv = 0, nx = 0;
@@ -140,7 +145,7 @@ __global__ void __launch_bounds__(kRedThreads) k_lrta_input(Geom g, const T* __r
       if (axis < 0) gl = l[i];
       else if (axis == 0) gl = l[base + (i0 + 1 < n0 ? i0 + 1 : 0)] - l[i];
       else gl = l[i + nx] - l[i];
-      X[i] = gl + lag[i] / (T)mu;
+      X[i] = gl + lag[i] * imu;
     }
   }
 }
@@ -190,6 +195,7 @@ __global__ void k_group_scale(Geom g, int structure, const T* __restrict__ mobs,
                               const uint8_t* __restrict__ mask, const T* __restrict__ l,
                               const T* __restrict__ y, double mu, double p0, double p1,
                               double level, double* __restrict__ scale) {
+  const T imu = (T)(1.0 / mu);
   const int64_t face = g.dims[0] * g.dims[1];
   const int64_t nf = g.N / face;
   if (structure == 1) {
@@ -198,7 +204,7 @@ __global__ void k_group_scale(Geom g, int structure, const T* __restrict__ mobs,
     double s2 = 0.0;
     for (int64_t f = 0; f < nf; ++f) {
       const int64_t i = t + face * f;
-      const double h = mask[i] ? (double)(mobs[i] - l[i] + y[i] / (T)mu) : 0.0;
+      const double h = mask[i] ? (double)(mobs[i] - l[i] + y[i] * imu) : 0.0;
       s2 += h * h;
     }
     const double gn = sqrt(s2);
@@ -209,7 +215,7 @@ __global__ void k_group_scale(Geom g, int structure, const T* __restrict__ mobs,
     double s2 = 0.0;
     for (int64_t e = threadIdx.x; e < face; e += blockDim.x) {
       const int64_t i = e + face * f;
-      const double h = mask[i] ? (double)(mobs[i] - l[i] + y[i] / (T)mu) : 0.0;
+      const double h = mask[i] ? (double)(mobs[i] - l[i] + y[i] * imu) : 0.0;
       s2 += h * h;
     }
     const double gn = sqrt(block_sum(s2, red));
@@ -259,11 +265,11 @@ __global__ void __launch_bounds__(kRedThreads) k_noise_dual(Geom g, const T* __r
   T v[7] = {T(0), T(0), T(0), T(0), T(0), T(0), T(0)};
   const int64_t face = g.dims[0] * g.dims[1];
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const T tmu = (T)mu, tlev = (T)level, tp0 = (T)p0;
+  const T tmu = (T)mu, tlev = (T)level, tp0 = (T)p0, timu = (T)(1.0 / mu);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.N; i += stride) {
     const T mi = mobs[i], li = l[i], yi = y[i], eo = e[i], lo = lold[i];
     const bool obs = mask[i] != 0;
-    const T h = mi - li + yi / tmu;
+    const T h = mi - li + yi * timu;
     T en;
     if (!obs) {
       en = h;

@@ -10,6 +10,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "lrta_kernels.cuh"
 #include "prox.cuh"
 
 namespace tr {
@@ -113,13 +114,14 @@ __global__ void __launch_bounds__(1024) k_face_svt(cplx* __restrict__ faces, int
         be = warp_sum(be);
         gr = warp_sum(gr);
         gi = warp_sum(gi);
-        const double g = sqrt(gr * gr + gi * gi);
+        const double g2 = gr * gr + gi * gi;
         // decoupled to working precision relative to the pair and to the face
-        if (!(g > 1e-15 * sqrt(al * be)) || !(g > 1e-17 * fnorm2)) continue;
-        const double zeta = (be - al) / (2.0 * g);
-        const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-        const cplx ph = {gr / g, gi / g};  // e^{i phi}
+        if (!(g2 > 1e-30 * al * be) || !(g2 > 1e-34 * fnorm2 * fnorm2) || !(g2 > 1e-300)) continue;
+        const double rg = (g2 > 1e-36 && g2 < 1e36) ? fast_rsqrt(g2) : 1.0 / sqrt(g2);
+        const double g = g2 * rg;
+        double c, s;
+        jacobi_cs(al, be, g, c, s);  // tau = (beta - alpha) / (2 |gamma|)
+        const cplx ph = {gr * rg, gi * rg};  // e^{i phi}
         // [xp, xq] <- [xp, xq] [[c, s e^{i phi}], [-s e^{-i phi}, c]]
         const cplx spn = {s * ph.re, s * ph.im};   // s e^{i phi}
         const cplx smn = {s * ph.re, -s * ph.im};  // s e^{-i phi}
@@ -139,6 +141,7 @@ __global__ void __launch_bounds__(1024) k_face_svt(cplx* __restrict__ faces, int
       }
       __syncthreads();
     }
+    if (threadIdx.x == 0) atomicAdd(&g_dbg[1], 1);  // face sweeps (summed over faces)
     if (!rot_any) break;
     __syncthreads();
   }

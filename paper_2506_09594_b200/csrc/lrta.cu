@@ -228,7 +228,8 @@ static int64_t panel(const T* A, int64_t m, int64_t n, int b, const T* P, const 
 }
 
 static void reduce(const double* part, int64_t nparts, int64_t len, double* out, cudaStream_t st) {
-  launch("reduce_partials", k_reduce_partials, (unsigned)cdiv(len, 256), 256, 0, st, part, (int)nparts, len, out);
+  launch("reduce_partials", k_reduce_partials, (unsigned)cdiv(len, 32), 256, 0, st, part,
+         (int)nparts, len, out);
 }
 
 // TSQR row-block size for an m x s Krylov block and the shared memory of each
@@ -344,7 +345,7 @@ static int bki_mode(const T* A, int64_t m, int64_t n, int r, int b, int q, Sketc
     }
     launch("ritz", k_ritz_warp<T>, 1, 256, sm, st, bf.M, s, bf.Z, m, r, V, F, Ft, info);
   } else {
-    launch("ritz", k_ritz<T>, 1, 1024, 2 * 64 * 65 * sizeof(double), st, bf.M, s, bf.Z, m, r, V,
+    launch("ritz", k_ritz<T>, 1, 512, 2 * 64 * 65 * sizeof(double), st, bf.M, s, bf.Z, m, r, V,
            F, Ft, info);
   }
   TR_LAUNCH_CHECK();
@@ -367,14 +368,14 @@ static int lrta_compress(const T* a, const Shape& sh, uint64_t seed, const T* g0
                   bf.F0t, bf.info, st))
     return 2;
   // core rows -> mode-1 unfolding (n2 x r0*nf), contiguous columns
-  launch("core_from_w", k_core_from_w<T, T>, (unsigned)cdiv(nA0 * sh.r0, 256), 256, 0, st, 
+  launch("core_from_w", k_core_from_w<T, T>, (unsigned)cdiv(nA0, 256), 256, 0, st,
       bf.W, nA0, (int)sh.s0, bf.V0, (int)sh.r0, sh.n2, bf.A1);
   // mode 1 on the core (m = n2, n = r0 * nf); logical columns use r0_eff
   SketchSpec sk1{seed, 1, sh.r0, bf.info + 1};
   if (bki_mode<T>(bf.A1, sh.n2, nA1, (int)sh.r1, (int)sh.b1, (int)sh.q1, sk1, g1, bf, bf.V1,
                   bf.F1, bf.F1t, bf.info + 2, st))
     return 2;
-  launch("core_from_w", k_core_from_w<T, double>, (unsigned)cdiv(nA1 * sh.r1, 256), 256, 0, st, 
+  launch("core_from_w", k_core_from_w<T, double>, (unsigned)cdiv(nA1, 256), 256, 0, st,
       bf.W, nA1, (int)sh.s1, bf.V1, (int)sh.r1, sh.r0, bf.core);
   TR_LAUNCH_CHECK();
   return 0;
@@ -772,3 +773,12 @@ int tr_profile_read(char* names, int64_t names_len, double* ms, int64_t* counts,
 }
 
 }  // extern "C"
+
+extern "C" int tr_debug_read(int* out, int reset) {
+  cudaDeviceSynchronize();
+  for (int i = 0; i < 8; ++i) {
+    out[i] = tr::g_dbg[i];
+    if (reset) tr::g_dbg[i] = 0;
+  }
+  return 0;
+}

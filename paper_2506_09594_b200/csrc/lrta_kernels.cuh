@@ -140,14 +140,65 @@ __global__ void __launch_bounds__(256) k_wtw(const T* __restrict__ W, int64_t n,
   }
 }
 
-// out[e] = sum_p part[p*len + e]  (fixed summation order: deterministic)
-__global__ void k_reduce_partials(const double* __restrict__ part, int nparts, int64_t len,
-                                  double* __restrict__ out) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= len) return;
+// out[e] = sum_p part[p*len + e]  (fixed summation order: deterministic).
+// One warp per 32 consecutive outputs x 8 partial groups: lanes stream
+// coalesced rows, each warp owns a slice of the partials, smem tree at the end.
+__global__ void __launch_bounds__(256) k_reduce_partials(const double* __restrict__ part,
+                                                         int nparts, int64_t len,
+                                                         double* __restrict__ out) {
+  __shared__ double acc[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t e = (int64_t)blockIdx.x * 32 + lane;
   double s = 0.0;
-  for (int p = 0; p < nparts; ++p) s += part[(int64_t)p * len + e];
-  out[e] = s;
+  if (e < len)
+    for (int p = warp; p < nparts; p += 8) s += part[(int64_t)p * len + e];
+  acc[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && e < len) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += acc[w][lane];
+    out[e] = t;
+  }
+}
+
+// Fast fp64 reciprocal / reciprocal square root: fp32 seed + two Newton steps
+// (~1 ulp; the IEEE-rounded slow paths dominate Jacobi round latency otherwise).
+// Valid for |x| in the fp32 normal range, which the callers guarantee.
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r = (double)__frcp_rn((float)x);
+  r = r * (2.0 - x * r);
+  r = r * (2.0 - x * r);
+  return r;
+}
+__device__ __forceinline__ double fast_rsqrt(double x) {
+  double r = (double)rsqrtf((float)x);
+  r = r * (1.5 - 0.5 * x * r * r);
+  r = r * (1.5 - 0.5 * x * r * r);
+  r = r * (1.5 - 0.5 * x * r * r);
+  return r;
+}
+
+// Jacobi rotation (c, s) annihilating a_pq of [[app, apq], [apq, aqq]]
+// (t = sign(tau) / (|tau| + sqrt(1 + tau^2)), tau = (aqq - app) / (2 apq)).
+__device__ __forceinline__ void jacobi_cs(double app, double aqq, double apq, double& c,
+                                          double& s) {
+  const double ra = fabs(apq);
+  const double inv = (ra > 1e-30 && ra < 1e30) ? fast_rcp(apq) : 1.0 / apq;
+  const double tau = (aqq - app) * 0.5 * inv;
+  double t;
+  const double at = fabs(tau);
+  if (at > 1e15) {
+    t = 0.5 / tau;  // sqrt(1 + tau^2) ~ |tau|
+  } else if (at < 1e-30) {
+    t = 1.0;
+  } else {
+    const double h = 1.0 + tau * tau;
+    const double sq = h * fast_rsqrt(h);
+    t = (tau >= 0 ? 1.0 : -1.0) * fast_rcp(at + sq);
+  }
+  c = fast_rsqrt(1.0 + t * t);
+  s = t * c;
 }
 
 // Krylov piece normalisation (sketch.py:257-258): piece = blk / ||blk||_F.
@@ -273,7 +324,7 @@ __global__ void __launch_bounds__(1024) k_orth(const double* __restrict__ K, int
 // cyclic Jacobi, descending order, F = Z V; then the canonical sign (largest
 // |entry| of every factor column positive, first index on ties).
 template <typename T>
-__global__ void __launch_bounds__(1024) k_ritz(const double* __restrict__ Mfull, int s,
+__global__ void __launch_bounds__(512) k_ritz(const double* __restrict__ Mfull, int s,
                                               const double* __restrict__ Z, int64_t m, int r,
                                               double* __restrict__ V, double* __restrict__ F,
                                               T* __restrict__ Ft, int64_t* __restrict__ info) {
@@ -318,10 +369,7 @@ __global__ void __launch_bounds__(1024) k_ritz(const double* __restrict__ Mfull,
           // pair and to ||M|| (rotating rounding noise never converges)
           if (fabs(apq) > 1e-15 * sqrt(fabs(app * aqq)) && fabs(apq) > 1e-16 * mnorm) {
             rot_any = 1;
-            const double tau = (aqq - app) / (2.0 * apq);
-            const double t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-            c = 1.0 / sqrt(1.0 + t * t);
-            sn = t * c;
+            jacobi_cs(app, aqq, apq, c, sn);
           }
         }
         pp[threadIdx.x] = p;
@@ -364,6 +412,7 @@ __global__ void __launch_bounds__(1024) k_ritz(const double* __restrict__ Mfull,
     __syncthreads();
     if (threadIdx.x == 0) rot_any = 0;
     __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(&g_dbg[0], 1);  // ritz sweeps
     if (!any) break;
   }
   // descending order (stable on ties, like reversing eigh's ascending output)
@@ -384,16 +433,32 @@ __global__ void __launch_bounds__(1024) k_ritz(const double* __restrict__ Mfull,
   }
   __syncthreads();
   const int re = min(r, n);
-  // F = Z V (m x r)
-  for (int64_t e = threadIdx.x; e < m * r; e += blockDim.x) {
-    const int64_t i = e % m;
-    const int k = (int)(e / m);
-    double f = 0.0;
-    if (k < re) {
-      const int col = order[k];
-      for (int j = 0; j < n; ++j) f += Z[i + m * j] * Q[j + ld * col];
+  // F = Z V (m x r): one row of Z per thread, held in registers (independent loads)
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    if (n <= 32) {
+      double z[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) z[j] = j < n ? Z[i + m * j] : 0.0;
+      for (int k = 0; k < r; ++k) {
+        double f = 0.0;
+        if (k < re) {
+          const int col = order[k];
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < n) f += z[j] * Q[j + ld * col];
+        }
+        F[i + m * k] = f;
+      }
+    } else {
+      for (int k = 0; k < r; ++k) {
+        double f = 0.0;
+        if (k < re) {
+          const int col = order[k];
+          for (int j = 0; j < n; ++j) f += Z[i + m * j] * Q[j + ld * col];
+        }
+        F[i + m * k] = f;
+      }
     }
-    F[e] = f;
   }
   __syncthreads();
   // canonical sign: one warp per column, argmax |F| with first-index ties
@@ -438,21 +503,29 @@ __global__ void __launch_bounds__(1024) k_ritz(const double* __restrict__ Mfull,
 
 // core rows from W: out[lo + inner*(i + r*f)] = sum_j W[c*s + j] V[j + s*i],
 // c = lo + inner * f.  Realises F^T A (sketch.py:267-269) without another pass.
+// One thread per unfolding column c: its W row (s values) times V (s x r,
+// in shared memory) gives the r core entries of that column.
 template <typename T, typename TO>
-__global__ void k_core_from_w(const T* __restrict__ W, int64_t n, int s,
-                              const double* __restrict__ V, int r, int64_t inner,
-                              TO* __restrict__ out) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t total = n * r;
-  if (t >= total) return;
-  const int64_t lo = t % inner;
-  const int64_t rest = t / inner;
-  const int i = (int)(rest % r);
-  const int64_t f = rest / r;
-  const int64_t c = lo + inner * f;
-  double acc = 0.0;
-  for (int j = 0; j < s; ++j) acc += (double)W[c * s + j] * V[j + (int64_t)s * i];
-  out[t] = (TO)acc;
+__global__ void __launch_bounds__(256) k_core_from_w(const T* __restrict__ W, int64_t n, int s,
+                                                     const double* __restrict__ V, int r,
+                                                     int64_t inner, TO* __restrict__ out) {
+  __shared__ double vs[64 * 64];
+  for (int e = threadIdx.x; e < s * r; e += blockDim.x) vs[e] = V[e];
+  __syncthreads();
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const int64_t lo = c % inner, f = c / inner;
+  double w[64];
+#pragma unroll
+  for (int j = 0; j < 64; ++j)
+    if (j < s) w[j] = (double)W[c * s + j];
+  for (int i = 0; i < r; ++i) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < 64; ++j)
+      if (j < s) acc += w[j] * vs[j + s * i];
+    out[lo + inner * (i + (int64_t)r * f)] = (TO)acc;
+  }
 }
 
 // C1[a + r0*(i2 + n2*f)] = sum_b core[a + r0*(b + r1*f)] * F1[i2 + n2*b]
