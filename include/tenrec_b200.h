@@ -134,6 +134,21 @@ int tr_admm_destroy(void* handle);
 /* The solver's main cudaStream_t (every sweep starts and ends on it). */
 void* tr_admm_stream(void* handle);
 
+/*
+ * Gradient system -- replaces tenrec.gradient.GradientSet (gradient.py:44-87)
+ * and solve_grad_system (gradient.py:90-106): out = (I + sum_k D_k^T D_k)^{-1}
+ * (b + sum_k D_k^T grads[k]), D_k the forward circular difference along mode
+ * modes[k].  The plan holds the FFT twiddles and the eigenvalue tables
+ * 4 sin^2(pi j / n); b, grads[k] (one per mode, in `modes` order) and out are
+ * device arrays of prod(dims) values in the plan's dtype, first axis fastest.
+ * order in [3, 8]; modes distinct.  Destroy with tr_gradsys_destroy.
+ */
+int tr_gradsys_create(int dtype, int order, const int64_t* dims, int nmodes, const int* modes,
+                      void** handle);
+int tr_gradsys_solve(void* handle, const void* b, const void* const* grads, void* out,
+                     void* stream);
+int tr_gradsys_destroy(void* handle);
+
 /* Number of kernels this library has launched in the process (accounting). */
 int64_t tr_launch_count(void);
 

@@ -9,6 +9,7 @@ by hand-written sm_100a CUDA kernels behind the C ABI in
 
 from .penalties import (PENALTY_NAMES, L1, MCP, SCAD, CappedLq, Firm, LogPenalty, Lq, Penalty,
                         make_penalty)
+from .gradient import GradientSet, solve_grad_system
 from .onebit import (ObservationSet, data_fit_update, gnobhtc, gnobrhtc, naive_estimate,
                      onebit_observe)
 from .sketch import SketchConfig, TuckerFactors, gnhtsvt_randomized, rsthosvd_bki
@@ -22,5 +23,5 @@ __all__ = [
     "make_penalty", "SketchConfig", "TuckerFactors", "gnhtsvt_randomized", "rsthosvd_bki",
     "DEFAULT_TRANSFORM", "Transform", "TransformError", "SolveReport", "SolverConfig",
     "default_lambda", "gnhtc", "gnrhtc", "ObservationSet", "data_fit_update", "gnobhtc",
-    "gnobrhtc", "naive_estimate", "onebit_observe",
+    "gnobrhtc", "naive_estimate", "onebit_observe", "GradientSet", "solve_grad_system",
 ]

@@ -44,6 +44,11 @@ SIGNATURES = {
     "tr_admm_read": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp]),
     "tr_admm_destroy": (ctypes.c_int, [_vp]),
     "tr_admm_stream": (_vp, [_vp]),
+    "tr_gradsys_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _c_i64p, ctypes.c_int,
+                                         ctypes.POINTER(ctypes.c_int),
+                                         ctypes.POINTER(ctypes.c_void_p)]),
+    "tr_gradsys_solve": (ctypes.c_int, [_vp, _vp, ctypes.POINTER(ctypes.c_void_p), _vp, _vp]),
+    "tr_gradsys_destroy": (ctypes.c_int, [_vp]),
     "tr_launch_count": (ctypes.c_int64, []),
     "tr_profile_enable": (ctypes.c_int, [ctypes.c_int]),
     "tr_profile_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int64, _c_dp, _c_i64p,

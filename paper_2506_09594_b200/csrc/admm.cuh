@@ -9,6 +9,7 @@
 // own stream with its own workspace, so the modes overlap on the GPU.
 #pragma once
 
+#include <limits>
 #include <vector>
 
 #include "admm_kernels.cuh"
@@ -31,6 +32,30 @@ struct AdmmConfig {
   double talphas[8];
 };
 
+// Solver buffers come from the device's stream-ordered pool with an unbounded
+// release threshold: memory freed by one solve stays reserved for the next, so
+// create/destroy of a multi-GB solver costs microseconds after the first run.
+// Allocation is ordered on the legacy stream; admm_create synchronises it
+// before the buffers are used on the solver's own streams.
+static int pool_alloc(void** p, size_t bytes) {
+  static bool ready[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && !ready[dev]) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    ready[dev] = true;
+  }
+  if (cudaMallocAsync(p, bytes, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return 1;
+  }
+  return 0;
+}
+
 template <typename T>
 struct Solver {
   AdmmConfig cfg;
@@ -50,7 +75,7 @@ struct Solver {
   int64_t ws_bytes = 0;
   std::vector<cudaStream_t> streams;
   std::vector<cudaEvent_t> evs;
-  cudaEvent_t ev_main;
+  cudaEvent_t ev_main = nullptr;
   SolveSpec ss;
   double mu;
   int64_t red_blocks;
@@ -59,16 +84,16 @@ struct Solver {
   template <typename X_>
   X_* alloc(int64_t n) {
     void* p = nullptr;
-    if (cudaMalloc(&p, std::max<int64_t>(n, 1) * sizeof(X_)) != cudaSuccess) return nullptr;
+    if (pool_alloc(&p, std::max<int64_t>(n, 1) * sizeof(X_))) return nullptr;
     allocs.push_back(p);
     return (X_*)p;
   }
   ~Solver() {
-    for (void* p : allocs) cudaFree(p);
+    for (void* p : allocs) cudaFreeAsync(p, 0);
     if (hres) cudaFreeHost(hres);
     for (auto s : streams) cudaStreamDestroy(s);
     for (auto e : evs) cudaEventDestroy(e);
-    cudaEventDestroy(ev_main);
+    if (ev_main) cudaEventDestroy(ev_main);
   }
   bool onebit() const { return cfg.kind >= 2; }
 };
@@ -98,6 +123,67 @@ static SpecGeom spec_geom(const Geom& g) {
   return sg;
 }
 
+template <typename T>
+using FftTileKernel = void (*)(const void*, void*, int, double, int64_t, int, int64_t, int64_t,
+                               const cpx<T>*, int, SolveSpec, const double*, int64_t);
+
+// k_fft_t instance for a 2^ln-point line (tile of 2048 points), or null
+template <typename T>
+static FftTileKernel<T> fft_tile_kernel(int ln) {
+  switch (ln) {
+    case 7: return k_fft_t<T, 7, 4>;
+    case 8: return k_fft_t<T, 8, 3>;
+    case 9: return k_fft_t<T, 9, 2>;
+    case 10: return k_fft_t<T, 10, 1>;
+    case 11: return k_fft_t<T, 11, 0>;
+    default: return nullptr;
+  }
+}
+
+// One persistent power-of-two pass (nt = points per line, 8 <= nt <= 2048):
+// the compile-time specialised kernel when the tile holds exactly 2048
+// points, the runtime-shaped k_fft_p2 otherwise.  Grid = resident CTAs.
+template <typename T>
+static void fft_pass_p2(int mode, const void* in, void* dst, double scale, int64_t stv, int n,
+                        int64_t hi, const cpx<T>* tw, int inverse, const SolveSpec& ss,
+                        const double* lam, int64_t tr_n1, cudaStream_t st) {
+  const int nt = mode == FFT_C2C ? n : n / 2;
+  int ln = 0;
+  while ((1 << ln) < nt) ++ln;
+  const int64_t cap = std::min<int64_t>(std::min<int64_t>(16, 2048 / nt), stv == 1 ? hi : stv);
+  int lL = 0;
+  while ((2ll << lL) <= cap) ++lL;  // largest power of two <= cap
+  const int64_t L = 1ll << lL;
+  const int64_t ntiles = stv == 1 ? cdiv(hi, L) : hi * cdiv(stv, L);
+  const size_t smem = ((size_t)nt + 2 * (size_t)L * (nt + 1)) * sizeof(cpx<T>);
+  static bool generic_only = getenv("TR_FFT_GENERIC") != nullptr;
+  static int occ[13] = {0};  // resident CTAs per SM, per specialised ln (index 12: k_fft_p2)
+  FftTileKernel<T> tk = (L * nt == 2048 && !generic_only) ? fft_tile_kernel<T>(ln) : nullptr;
+  const int slot = tk ? ln : 12;
+  if (occ[slot] == 0) {
+    const void* f = tk ? (const void*)tk : (const void*)k_fft_p2<T>;
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, f, 256, tk ? smem : 200 * 1024);
+    occ[slot] = std::max(1, b);
+  }
+  // k_fft_p2 smem varies per call: size its grid from this call's footprint
+  int per_sm = occ[slot];
+  if (!tk) {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_fft_p2<T>, 256, smem);
+    per_sm = std::max(1, b);
+  }
+  const int64_t grid = std::min<int64_t>(ntiles, (int64_t)per_sm * num_sms());
+  if (tk) {
+    launch("fft", tk, (unsigned)grid, 256, smem, st, in, dst, mode, scale, stv, n, hi, ntiles, tw,
+           inverse, ss, lam, tr_n1);
+  } else {
+    launch("fft", k_fft_p2<T>, (unsigned)grid, 256, smem, st, in, dst, mode, scale, stv, n, hi, lL,
+           ntiles, tw, inverse, ss, lam, tr_n1);
+  }
+}
+
 // forward FFT over all axes, diagonal solve in the last-axis pass, inverse FFT
 template <typename T>
 static int fft_solve(Solver<T>& s, const T* rhs, T* out, cudaStream_t st) {
@@ -121,20 +207,8 @@ static int fft_solve(Solver<T>& s, const T* rhs, T* out, cudaStream_t st) {
                             (mode != FFT_R2C || (n * (int64_t)sizeof(T)) % 16 == 0) &&
                             getenv("TR_FFT_SIMPLE") == nullptr;
     if (persistent) {
-      static bool pattr = false;
-      if (!pattr) {
-        cudaFuncSetAttribute(k_fft_p2<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        pattr = true;
-      }
-      const int64_t cap = std::min<int64_t>(std::min<int64_t>(16, 2048 / nt), stv == 1 ? hi : stv);
-      int lL = 0;
-      while ((2ll << lL) <= cap) ++lL;  // largest power of two <= cap
-      const int64_t L = 1ll << lL;
-      const int64_t ntiles = stv == 1 ? cdiv(hi, L) : hi * cdiv(stv, L);
-      const int64_t grid = std::min<int64_t>(ntiles, 2 * (int64_t)num_sms());
-      const size_t smem = ((size_t)nt + 2 * (size_t)L * (nt + 1)) * sizeof(cpx<T>);
-      launch("fft", k_fft_p2<T>, (unsigned)grid, 256, smem, st, in, dst, mode, scale, stv, n, hi,
-             lL, ntiles, (const cpx<T>*)s.tw[a], inverse, ss, (const double*)s.lam, (int64_t)0);
+      fft_pass_p2<T>(mode, in, dst, scale, stv, n, hi, (const cpx<T>*)s.tw[a], inverse, ss,
+                     (const double*)s.lam, 0, st);
       return 0;
     }
     // at most 4096 complex line elements per CTA (8 radix-2 groups per thread)
@@ -184,20 +258,7 @@ static int fft_c2c(const cpx<T>* tw, const double* lam, void* data, int n, int64
                    int inverse, const SolveSpec& ss, cudaStream_t st) {
   const bool pow2 = (n & (n - 1)) == 0;
   if (pow2 && n >= 8 && n <= 2048 && getenv("TR_FFT_SIMPLE") == nullptr) {
-    static bool pattr = false;
-    if (!pattr) {
-      cudaFuncSetAttribute(k_fft_p2<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      pattr = true;
-    }
-    const int64_t cap = std::min<int64_t>(std::min<int64_t>(16, 2048 / n), stv == 1 ? hi : stv);
-    int lL = 0;
-    while ((2ll << lL) <= cap) ++lL;
-    const int64_t L = 1ll << lL;
-    const int64_t ntiles = stv == 1 ? cdiv(hi, L) : hi * cdiv(stv, L);
-    const int64_t grid = std::min<int64_t>(ntiles, 2 * (int64_t)num_sms());
-    const size_t smem = ((size_t)n + 2 * (size_t)L * (n + 1)) * sizeof(cpx<T>);
-    launch("fft", k_fft_p2<T>, (unsigned)grid, 256, smem, st, (const void*)data, data,
-           (int)FFT_C2C, 1.0, stv, n, hi, lL, ntiles, tw, inverse, ss, lam, (int64_t)0);
+    fft_pass_p2<T>(FFT_C2C, data, data, 1.0, stv, n, hi, tw, inverse, ss, lam, 0, st);
     return 0;
   }
   static bool attr = false;
@@ -250,23 +311,11 @@ static int fft_solve2(Solver<T>& s, const T* rhs, T* out, cudaStream_t st) {
     off.lam_off[p] = on.lam_off[p] = s.ss.lam_off[orig[p]];
   }
   const cpx<T>* const* tw = (const cpx<T>* const*)s.tw.data();
-  static bool pattr = false;
-  if (!pattr) {
-    cudaFuncSetAttribute(k_fft_p2<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    pattr = true;
-  }
   // axis 0, real -> half spectrum (swapped layout)
   const int64_t lines = g.N / n0;
   auto r2c_like = [&](int mode, const void* in, void* dst, double scale) {
-    const int64_t cap = std::min<int64_t>(std::min<int64_t>(16, 2048 / hn), lines);
-    int lL = 0;
-    while ((2ll << lL) <= cap) ++lL;
-    const int64_t L = 1ll << lL;
-    const int64_t ntiles = cdiv(lines, L);
-    const int64_t grid = std::min<int64_t>(ntiles, 2 * (int64_t)num_sms());
-    const size_t smem = ((size_t)hn + 2 * (size_t)L * (hn + 1)) * sizeof(cpx<T>);
-    launch("fft", k_fft_p2<T>, (unsigned)grid, 256, smem, st, in, dst, mode, scale, (int64_t)1,
-           (int)n0, lines, lL, ntiles, tw[0], 0, off, (const double*)s.lam, n1);
+    fft_pass_p2<T>(mode, in, dst, scale, 1, (int)n0, lines, tw[0], 0, off, (const double*)s.lam, n1,
+                   st);
   };
   r2c_like(FFT_R2C, rhs, s.spec, 1.0);
   for (int p = 0; p < d - 1; ++p) {
@@ -557,6 +606,7 @@ static int admm_create(const AdmmConfig& cfg, int order, const int64_t* dims, co
       delete s;
       TR_REQUIRE(false, "device allocation failed (out of memory?)");
     }
+  TR_CUDA(cudaStreamSynchronize(0));  // pool allocations are ordered on the legacy stream
   TR_CUDA(cudaMallocHost(&s->hres, 128 * sizeof(double)));
   // LRTA workspaces, one per mode stream
   {
@@ -570,6 +620,7 @@ static int admm_create(const AdmmConfig& cfg, int order, const int64_t* dims, co
     TR_REQUIRE(p, "workspace allocation failed");
     s->ws.push_back(p);
   }
+  TR_CUDA(cudaStreamSynchronize(0));
   for (int k = 0; k <= nm; ++k) {
     cudaStream_t st;
     TR_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
@@ -606,6 +657,84 @@ static int admm_create(const AdmmConfig& cfg, int order, const int64_t* dims, co
   TR_CUDA(cudaStreamSynchronize(st));
   *out = s;
   return 0;
+}
+
+// Gradient-system plan: GradientSet (tenrec/gradient.py:44-87) + the solve of
+// solve_grad_system (gradient.py:90-106) on device buffers.  A Solver holding
+// only the geometry, twiddles, eigenvalue tables, spectrum and rhs buffers.
+template <typename T>
+static int gradsys_create(int order, const int64_t* dims, int nmodes, const int* modes,
+                          Solver<T>** out) {
+  TR_REQUIRE(order >= 3 && order <= kMaxOrder, "order must be in [3, %d]", kMaxOrder);
+  TR_REQUIRE(nmodes >= 1 && nmodes <= order, "gradient mode set must be nonempty");
+  for (int k = 0; k < nmodes; ++k) {
+    TR_REQUIRE(modes[k] >= 0 && modes[k] < order, "gradient mode %d out of range for order %d",
+               modes[k], order);
+    for (int j = 0; j < k; ++j) TR_REQUIRE(modes[j] != modes[k], "gradient mode %d repeated", modes[k]);
+  }
+  for (int i = 0; i < order; ++i) TR_REQUIRE(dims[i] >= 1, "dims must be positive");
+  auto* s = new Solver<T>();
+  s->order = order;
+  s->cfg.nmodes = nmodes;
+  for (int k = 0; k < nmodes; ++k) s->cfg.modes[k] = modes[k];
+  Geom& g = s->g;
+  g.d = order;
+  g.N = 1;
+  for (int i = 0; i < order; ++i) {
+    g.dims[i] = dims[i];
+    g.st[i] = g.N;
+    g.lst[i] = g.N / dims[0];
+    g.N *= dims[i];
+  }
+  s->rhs = s->template alloc<T>(g.N);
+  s->spec = s->template alloc<cpx<T>>(g.N);
+  int64_t lam_total = 0;
+  for (int i = 0; i < order; ++i) {
+    s->tw.push_back(s->template alloc<cpx<T>>(dims[i]));
+    lam_total += dims[i];
+  }
+  s->lam = s->template alloc<double>(lam_total);
+  for (void* p : s->allocs)
+    if (!p) {
+      delete s;
+      TR_REQUIRE(false, "device allocation failed (out of memory?)");
+    }
+  SolveSpec& ss = s->ss;
+  ss.active = 0;
+  ss.d = order;
+  int64_t off = 0;
+  for (int i = 0; i < order; ++i) {
+    ss.dims[i] = dims[i];
+    ss.lam_off[i] = -1;
+    launch("setup", k_twiddles<T>, (unsigned)cdiv(dims[i], 256), 256, 0, (cudaStream_t)0,
+           (int)dims[i], s->tw[i]);
+    launch("setup", k_lap_eig, (unsigned)cdiv(dims[i], 256), 256, 0, (cudaStream_t)0, (int)dims[i],
+           s->lam + off);
+    for (int k = 0; k < nmodes; ++k)
+      if (modes[k] == i) ss.lam_off[i] = off;
+    off += dims[i];
+  }
+  TR_LAUNCH_CHECK();
+  TR_CUDA(cudaStreamSynchronize(0));
+  *out = s;
+  return 0;
+}
+
+// out = (I + sum_k D_k^T D_k)^{-1} (b + sum_k D_k^T grads[k]).  The rhs is
+// formed by k_admm_rhs with mu = inf (its y / mu and lag / mu terms vanish).
+template <typename T>
+static int gradsys_solve(Solver<T>& s, const T* b, const T* const* grads, T* out, cudaStream_t st) {
+  ModePtrs<T> gm{}, lag{};
+  gm.count = lag.count = s.cfg.nmodes;
+  for (int k = 0; k < s.cfg.nmodes; ++k) {
+    TR_REQUIRE(grads[k], "null gradient term for mode %d", s.cfg.modes[k]);
+    gm.p[k] = lag.p[k] = const_cast<T*>(grads[k]);
+    gm.axis[k] = lag.axis[k] = s.cfg.modes[k];
+  }
+  const double inf = std::numeric_limits<double>::infinity();
+  launch("admm_rhs", k_admm_rhs<T>, (unsigned)grid_for<T>(s.g.N), kRedThreads, 0, st, s.g, b,
+         (const T*)nullptr, b, inf, gm, lag, s.rhs);
+  return fft_solve2<T>(s, s.rhs, out, st);
 }
 
 }  // namespace tr

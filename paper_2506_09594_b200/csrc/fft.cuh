@@ -766,6 +766,271 @@ __global__ void __launch_bounds__(256) k_fft_p2(const void* in, void* out,  // m
   }
 }
 
+// ---------------------------------------------------------------------------
+// Compile-time specialised pass: nt = 2^LN points, L = 2^LL lines, L*nt = 2048
+// (8 points per thread of 256).  Every shift, mask, group count and twiddle
+// offset is a constant, so the stages unroll into straight-line code.
+// ---------------------------------------------------------------------------
+template <typename T, int LN, int LL>
+__device__ __forceinline__ void stockham_t(cpx<T>* buf, const cpx<T>* st_tab, bool inverse,
+                                           bool lo_major) {
+  constexpr int TOT = 1 << (LN + LL);
+  constexpr int NST = (LN + 1) / 2;
+#pragma unroll
+  for (int s = 0; s < NST; ++s) {
+    const int lNs = 2 * s;
+    const int lR = (LN - lNs) >= 2 ? 2 : 1;
+    const int lg = LN - lR;
+    const int GPT = (TOT >> lR) / 256;  // groups per thread
+    const int toff = (1 << (2 * s)) - 1;  // sum over previous radix-4 stages of Ns * 3
+    const int nsm = (1 << lNs) - 1;
+    cpx<T> v[4][4];
+#pragma unroll
+    for (int g = 0; g < GPT; ++g) {
+      const int e = threadIdx.x + g * 256;
+      const int l = lo_major ? (e & ((1 << LL) - 1)) : (e >> lg);
+      const int j = lo_major ? (e >> LL) : (e & ((1 << lg) - 1));
+      const int jm = j & nsm;
+#pragma unroll
+      for (int r = 0; r < (1 << lR); ++r) {
+        const int k = j + (r << lg);
+        cpx<T> x = buf[lo_major ? (k << LL) + l : (l << LN) + k];
+        if (r > 0 && s > 0) {
+          cpx<T> w = st_tab[toff + jm * ((1 << lR) - 1) + r - 1];
+          if (inverse) w.im = -w.im;
+          x = cmulc(x, w);
+        }
+        v[g][r] = x;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int g = 0; g < GPT; ++g) {
+      const int e = threadIdx.x + g * 256;
+      const int l = lo_major ? (e & ((1 << LL) - 1)) : (e >> lg);
+      const int j = lo_major ? (e >> LL) : (e & ((1 << lg) - 1));
+      const int base = ((j >> lNs) << (lNs + lR)) + (j & nsm);
+      auto at = [&](int r) -> cpx<T>& {
+        const int k = base + (r << lNs);
+        return buf[lo_major ? (k << LL) + l : (l << LN) + k];
+      };
+      if (lR == 2) {
+        const cpx<T> a0 = cadd(v[g][0], v[g][2]), a1 = csub(v[g][0], v[g][2]);
+        const cpx<T> a2 = cadd(v[g][1], v[g][3]);
+        const cpx<T> d = csub(v[g][1], v[g][3]);
+        const cpx<T> a3 = inverse ? cpx<T>{-d.im, d.re} : cpx<T>{d.im, -d.re};
+        at(0) = cadd(a0, a2);
+        at(1) = cadd(a1, a3);
+        at(2) = csub(a0, a2);
+        at(3) = csub(a1, a3);
+      } else {
+        at(0) = cadd(v[g][0], v[g][1]);
+        at(1) = csub(v[g][0], v[g][1]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <typename T, int LN, int LL>
+__global__ void __launch_bounds__(256, 2) k_fft_t(const void* in, void* out,  // may alias
+                                               int mode, double out_scale, int64_t st, int n,
+                                               int64_t hi, int64_t ntiles,
+                                               const cpx<T>* __restrict__ tw, int inverse,
+                                               SolveSpec ss, const double* __restrict__ lam,
+                                               int64_t tr_n1) {
+  constexpr int NT = 1 << LN, L = 1 << LL, TOT = NT * L, PER = TOT / 256;
+  static_assert(TOT == 2048, "tile must hold 2048 points");
+  extern __shared__ __align__(16) unsigned char fft_smem[];
+  const int hn = n / 2;
+  const int bufc = L * (NT + 1);
+  const T osc = (T)out_scale;
+  cpx<T>* ts = reinterpret_cast<cpx<T>*>(fft_smem);
+  cpx<T>* const buf0 = ts + NT;
+  __shared__ double denl[16];
+  __shared__ int64_t lbase[16];
+  build_stage_twiddles<T>(ts, LN, tw, (mode == FFT_C2C) ? 1 : 2);
+  const bool lo_lines = st > 1;
+  const int64_t nlob = lo_lines ? (st + L - 1) >> LL : 1;
+  auto origin = [&](int64_t t, int64_t& lo0, int64_t& hi0) {
+    if (!lo_lines) {
+      lo0 = 0;
+      hi0 = t << LL;
+    } else {
+      lo0 = (t % nlob) << LL;
+      hi0 = t / nlob;
+    }
+  };
+  const int tid = threadIdx.x;
+  auto load = [&](int64_t t, int b) {
+    if (t < ntiles) {
+      int64_t lo0, hi0;
+      origin(t, lo0, hi0);
+      const uint32_t sb = (uint32_t)__cvta_generic_to_shared(buf0 + b * bufc);
+      if (mode == FFT_R2C) {
+        const int64_t lines = (hi - hi0) < L ? (hi - hi0) : L;
+        const unsigned char* src =
+            reinterpret_cast<const unsigned char*>(in) + hi0 * n * (int64_t)sizeof(T);
+        const int64_t bytes = lines * n * (int64_t)sizeof(T);
+        for (int64_t o = tid * 16; o < bytes; o += 256 * 16) cpa16(sb + (uint32_t)o, src + o);
+      } else if (mode == FFT_C2R) {
+        // swapped layout (tr_n1) or plain; thread serves line l = tid mod L
+        const cpx<T>* X = reinterpret_cast<const cpx<T>*>(in);
+        const int l = tid & (L - 1);
+        const int64_t line = hi0 + l;
+        if (line < hi) {
+          const int64_t gb = tr_n1 ? (line % tr_n1) + tr_n1 * (int64_t)(hn + 1) * (line / tr_n1)
+                                   : line * (hn + 1);
+          const int64_t kst = tr_n1 ? tr_n1 : 1;
+          for (int k = tid >> LL; k <= hn; k += 256 >> LL) {
+            const uint32_t d = sb + (uint32_t)((l * (hn + 1) + k) * (int)sizeof(cpx<T>));
+            if (sizeof(cpx<T>) == 8) cpa8(d, X + gb + kst * k);
+            else cpa16(d, X + gb + kst * k);
+          }
+        }
+      } else {
+        const cpx<T>* src = reinterpret_cast<const cpx<T>*>(in);
+        if (lo_lines) {
+          // element (l, k) at lo0 + l + st (k + n hi0); thread: l = tid & (L-1), k = (tid >> LL) + u * (256 >> LL)
+          const int l = tid & (L - 1);
+          if (lo0 + l < st) {
+            const cpx<T>* p = src + lo0 + l + st * ((int64_t)n * hi0);
+#pragma unroll
+            for (int u = 0; u < PER; ++u) {
+              const int k = (tid >> LL) + u * (256 >> LL);
+              const uint32_t d = sb + (uint32_t)(((k << LL) + l) * (int)sizeof(cpx<T>));
+              if (sizeof(cpx<T>) == 8) cpa8(d, p + st * k);
+              else cpa16(d, p + st * k);
+            }
+          }
+        } else {
+          // L contiguous lines of NT points: one contiguous block
+          const int64_t lines = (hi - hi0) < L ? (hi - hi0) : L;
+          const cpx<T>* p = src + hi0 * NT;
+#pragma unroll
+          for (int u = 0; u < PER; ++u) {
+            const int e = tid + u * 256;
+            if ((e >> LN) < lines) {
+              const uint32_t d = sb + (uint32_t)(e * (int)sizeof(cpx<T>));
+              if (sizeof(cpx<T>) == 8) cpa8(d, p + e);
+              else cpa16(d, p + e);
+            }
+          }
+        }
+      }
+    }
+    cpa_commit();
+  };
+  int64_t t = blockIdx.x;
+  load(t, 0);
+  int b = 0;
+  for (; t < ntiles; t += gridDim.x, b ^= 1) {
+    load(t + gridDim.x, b ^ 1);
+    cpa_wait1();
+    int64_t lo0, hi0;
+    origin(t, lo0, hi0);
+    if (ss.active && tid < L) {
+      double den = 1.0;
+      int64_t rem = lo0 + tid;
+      for (int a = 0; a < ss.d - 1; ++a) {
+        const int64_t j = rem % ss.dims[a];
+        rem /= ss.dims[a];
+        if (ss.lam_off[a] >= 0) den += lam[ss.lam_off[a] + j];
+      }
+      denl[tid] = den;
+    }
+    if (mode == FFT_R2C && tid < L) {
+      const int64_t line = hi0 + tid;
+      lbase[tid] = tr_n1 ? (line % tr_n1) + tr_n1 * (int64_t)(hn + 1) * (line / tr_n1)
+                         : line * (hn + 1);
+    }
+    __syncthreads();
+    cpx<T>* buf = buf0 + b * bufc;
+    if (mode == FFT_C2R) {
+      cpx<T> zv[PER];
+#pragma unroll
+      for (int c = 0; c < PER; ++c) {
+        const int e = tid + c * 256;
+        const int l = e >> LN, k = e & (NT - 1);
+        const cpx<T> a = buf[l * (hn + 1) + k], bb = cconjt(buf[l * (hn + 1) + hn - k]);
+        const cpx<T> E = {(a.re + bb.re) * T(0.5), (a.im + bb.im) * T(0.5)};
+        cpx<T> w = tw[k];
+        w.im = -w.im;
+        const cpx<T> D = {(a.re - bb.re) * T(0.5), (a.im - bb.im) * T(0.5)};
+        const cpx<T> O = cmulc(D, w);
+        zv[c] = {E.re - O.im, E.im + O.re};
+      }
+      __syncthreads();
+#pragma unroll
+      for (int c = 0; c < PER; ++c) buf[tid + c * 256] = zv[c];
+      __syncthreads();
+    }
+    stockham_t<T, LN, LL>(buf, ts, (mode == FFT_C2R) || inverse != 0, lo_lines);
+    if (ss.active) {
+      const int lo_off = ss.lam_off[ss.d - 1];
+#pragma unroll
+      for (int c = 0; c < PER; ++c) {
+        const int e = tid + c * 256;
+        const int l = lo_lines ? (e & (L - 1)) : (e >> LN);
+        const int k = lo_lines ? (e >> LL) : (e & (NT - 1));
+        const double den = denl[l] + (lo_off >= 0 ? lam[lo_off + k] : 0.0);
+        const T inv = (T)(1.0 / den);
+        const cpx<T> v = buf[e];
+        buf[e] = {v.re * inv, v.im * inv};
+      }
+      __syncthreads();
+      stockham_t<T, LN, LL>(buf, ts, true, lo_lines);
+    }
+    if (mode == FFT_R2C) {
+      cpx<T>* Xo = reinterpret_cast<cpx<T>*>(out);
+      const int64_t kst = tr_n1 ? tr_n1 : 1;
+      const int l = tid & (L - 1);
+      if (hi0 + l < hi) {
+        for (int k = tid >> LL; k <= hn; k += 256 >> LL) {
+          const cpx<T> a = buf[(l << LN) + (k & (NT - 1))];
+          const cpx<T> bb = cconjt(buf[(l << LN) + ((NT - k) & (NT - 1))]);
+          const cpx<T> E = {(a.re + bb.re) * T(0.5), (a.im + bb.im) * T(0.5)};
+          const cpx<T> D = {(a.re - bb.re) * T(0.5), (a.im - bb.im) * T(0.5)};
+          const cpx<T> O = {D.im, -D.re};
+          Xo[lbase[l] + kst * k] = cadd(E, cmulc(tw[k], O));
+        }
+      }
+    } else if (mode == FFT_C2R) {
+#pragma unroll
+      for (int c = 0; c < PER; ++c) {
+        const int e = tid + c * 256;
+        const int l = e >> LN, k = e & (NT - 1);
+        const int64_t line = hi0 + l;
+        if (line < hi) {
+          const cpx<T> v = buf[e];
+          reinterpret_cast<cpx<T>*>(out)[line * NT + k] = {v.re * osc, v.im * osc};  // x[2k], x[2k+1]
+        }
+      }
+    } else if (lo_lines) {
+      const int l = tid & (L - 1);
+      if (lo0 + l < st) {
+        cpx<T>* p = reinterpret_cast<cpx<T>*>(out) + lo0 + l + st * ((int64_t)n * hi0);
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int k = (tid >> LL) + u * (256 >> LL);
+          const cpx<T> v = buf[(k << LL) + l];
+          p[st * k] = {v.re * osc, v.im * osc};
+        }
+      }
+    } else {
+      const int64_t lines = (hi - hi0) < L ? (hi - hi0) : L;
+      cpx<T>* p = reinterpret_cast<cpx<T>*>(out) + hi0 * NT;
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
+        const int e = tid + u * 256;
+        const cpx<T> v = buf[e];
+        if ((e >> LN) < lines) p[e] = {v.re * osc, v.im * osc};
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // real <-> complex conversion for the full-spectrum fallback (odd n0)
 template <typename T>
 __global__ void k_real_to_cpx(const T* __restrict__ x, cpx<T>* __restrict__ z, int64_t N) {

@@ -698,6 +698,42 @@ int tr_admm_destroy(void* handle) {
   return 0;
 }
 
+int tr_gradsys_create(int dtype, int order, const int64_t* dims, int nmodes, const int* modes,
+                      void** handle) {
+  TR_REQUIRE(dtype == TR_F32 || dtype == TR_F64, "dtype must be TR_F32 or TR_F64");
+  TR_REQUIRE(dims && modes && handle, "null pointer argument");
+  auto* h = new AdmmHandle{dtype, nullptr};
+  int rc;
+  if (dtype == TR_F32) {
+    Solver<float>* s = nullptr;
+    rc = gradsys_create<float>(order, dims, nmodes, modes, &s);
+    h->solver = s;
+  } else {
+    Solver<double>* s = nullptr;
+    rc = gradsys_create<double>(order, dims, nmodes, modes, &s);
+    h->solver = s;
+  }
+  if (rc) {
+    delete h;
+    return rc;
+  }
+  *handle = h;
+  return 0;
+}
+
+int tr_gradsys_solve(void* handle, const void* b, const void* const* grads, void* out,
+                     void* stream) {
+  TR_REQUIRE(handle && b && grads && out, "null pointer argument");
+  auto* h = (AdmmHandle*)handle;
+  if (h->dtype == TR_F32)
+    return gradsys_solve<float>(*(Solver<float>*)h->solver, (const float*)b,
+                                (const float* const*)grads, (float*)out, (cudaStream_t)stream);
+  return gradsys_solve<double>(*(Solver<double>*)h->solver, (const double*)b,
+                               (const double* const*)grads, (double*)out, (cudaStream_t)stream);
+}
+
+int tr_gradsys_destroy(void* handle) { return tr_admm_destroy(handle); }
+
 int tr_prox(int dtype, int penalty_kind, double p0, double p1, double mu, const void* v,
             void* out, int64_t n, void* stream) {
   TR_REQUIRE(penalty_kind >= 0 && penalty_kind <= 6, "bad penalty kind %d", penalty_kind);

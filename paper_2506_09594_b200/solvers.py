@@ -25,7 +25,7 @@ from . import _lib
 from .penalties import MCP, Penalty
 from .penalties import encode as encode_penalty
 from .sketch import SketchConfig
-from .tensors import ColMajor, from_device, to_device
+from .tensors import ColMajor, from_device, mask_to_device, to_device
 from .transform import DEFAULT_TRANSFORM, Transform, as_transform
 
 __all__ = ["SolverConfig", "SolveReport", "default_lambda", "gnrhtc", "gnhtc", "RESIDUAL_NAMES"]
@@ -178,13 +178,7 @@ class NativeSolver:
 
 
 def _mask_device(mask, dims):
-    import torch
-
-    if isinstance(mask, torch.Tensor):
-        m = mask.to(device="cuda", dtype=torch.uint8)
-        return m.permute(*reversed(range(m.dim()))).contiguous().reshape(-1)
-    m = np.asarray(mask, dtype=bool)
-    return torch.from_numpy(np.ascontiguousarray(m.ravel(order="F")).astype(np.uint8)).to("cuda")
+    return mask_to_device(mask)
 
 
 def _admm_complete(mobs, mask, cfg: SolverConfig, noise_free: bool):

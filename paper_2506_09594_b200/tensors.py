@@ -45,6 +45,30 @@ def _torch():
     return torch
 
 
+def _upload(a: np.ndarray):
+    """Flat column-major CUDA copy of a numpy array.
+
+    F-ordered arrays go up as they are; anything else goes up in C order (one
+    contiguous host pass at most) and is transposed on the device -- a host
+    ``ravel(order="F")`` of a C-ordered array is a strided gather that costs
+    seconds at these sizes.  The host side goes through torch's cached
+    page-locked buffers so the DMA runs at full PCIe/C2C speed.
+    """
+    torch = _torch()
+    fortran = a.flags.f_contiguous
+    if not fortran:
+        a = np.ascontiguousarray(a)
+    raw = a.view(np.uint8) if a.dtype == np.bool_ else a
+    host = torch.from_numpy(raw.ravel(order="F" if fortran else "C"))
+    if host.numel():
+        dev = host.pin_memory().to("cuda", non_blocking=True)
+    else:
+        dev = host.to("cuda")
+    if not fortran and a.ndim > 1:
+        dev = dev.reshape(a.shape).permute(*reversed(range(a.ndim))).contiguous().reshape(-1)
+    return dev
+
+
 def to_device(x, dtype=None) -> ColMajor:
     """Column-major CUDA copy of ``x`` (numpy array, scalar list or torch tensor)."""
     torch = _torch()
@@ -62,9 +86,16 @@ def to_device(x, dtype=None) -> ColMajor:
     else:
         np_dtype = np.float32 if dtype == torch.float32 else np.float64
     a = a.astype(np_dtype, copy=False)
-    host = torch.from_numpy(np.ascontiguousarray(a.ravel(order="F")))
-    flat = host.pin_memory().to("cuda", non_blocking=True) if host.numel() else host.to("cuda")
-    return ColMajor(flat, a.shape, "numpy", np_dtype)
+    return ColMajor(_upload(a), a.shape, "numpy", np_dtype)
+
+
+def mask_to_device(mask):
+    """Observation mask as a flat column-major uint8 CUDA buffer."""
+    torch = _torch()
+    if isinstance(mask, torch.Tensor):
+        m = mask.to(device="cuda", dtype=torch.uint8)
+        return m.permute(*reversed(range(m.dim()))).contiguous().reshape(-1)
+    return _upload(np.asarray(mask, dtype=bool))
 
 
 def empty_like(cm: ColMajor, dims=None) -> ColMajor:
@@ -75,9 +106,20 @@ def empty_like(cm: ColMajor, dims=None) -> ColMajor:
 
 
 def from_device(cm: ColMajor):
-    """Back to the caller's container: numpy (same dtype) or a CUDA tensor view."""
+    """Back to the caller's container: numpy (same dtype) or a CUDA tensor view.
+
+    numpy results are returned in page-locked memory from torch's caching host
+    allocator (one DMA, no extra host copy; the block is recycled once the
+    array is dropped).
+    """
+    torch = _torch()
     if cm.kind == "numpy":
-        return cm.flat.cpu().numpy().reshape(cm.dims, order="F")
+        if cm.flat.numel() == 0:
+            return np.zeros(cm.dims, dtype=cm.np_dtype, order="F")
+        host = torch.empty(cm.flat.numel(), dtype=cm.flat.dtype, pin_memory=True)
+        host.copy_(cm.flat, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return host.numpy().reshape(cm.dims, order="F")
     d = len(cm.dims)
     return cm.flat.reshape(tuple(reversed(cm.dims))).permute(*reversed(range(d)))
 
