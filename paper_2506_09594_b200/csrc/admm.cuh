@@ -155,10 +155,11 @@ static void fft_pass_p2(int mode, const void* in, void* dst, double scale, int64
   while ((2ll << lL) <= cap) ++lL;  // largest power of two <= cap
   const int64_t L = 1ll << lL;
   const int64_t ntiles = stv == 1 ? cdiv(hi, L) : hi * cdiv(stv, L);
-  const size_t smem = ((size_t)nt + 2 * (size_t)L * (nt + 1)) * sizeof(cpx<T>);
   static bool generic_only = getenv("TR_FFT_GENERIC") != nullptr;
   static int occ[13] = {0};  // resident CTAs per SM, per specialised ln (index 12: k_fft_p2)
   FftTileKernel<T> tk = (L * nt == 2048 && !generic_only) ? fft_tile_kernel<T>(ln) : nullptr;
+  const size_t smem = tk ? ((size_t)nt + 2 * (size_t)kFftTileSlots) * sizeof(cpx<T>)
+                         : ((size_t)nt + 2 * (size_t)L * (nt + 1)) * sizeof(cpx<T>);
   const int slot = tk ? ln : 12;
   if (occ[slot] == 0) {
     const void* f = tk ? (const void*)tk : (const void*)k_fft_p2<T>;

@@ -768,64 +768,127 @@ __global__ void __launch_bounds__(256) k_fft_p2(const void* in, void* out,  // m
 
 // ---------------------------------------------------------------------------
 // Compile-time specialised pass: nt = 2^LN points, L = 2^LL lines, L*nt = 2048
-// (8 points per thread of 256).  Every shift, mask, group count and twiddle
-// offset is a constant, so the stages unroll into straight-line code.
+// (8 points per thread of 256).  Stockham stages of radix 8 (radix 4 where
+// log2 nt is not a multiple of 3: 128 = 8.4.4, 1024 = 8.8.4.4, 2048 = 8.8.8.4),
+// each thread running 8/R register butterflies per stage, so a 512-point line
+// takes 3 shared-memory exchanges instead of 5.  Tile slots are padded by one
+// per 16 (fpad) which makes the stride-Ns Stockham writes bank-conflict free.
+// Shapes, shifts, twiddle offsets are constants: the stages unroll into
+// straight-line code.
 // ---------------------------------------------------------------------------
-template <typename T, int LN, int LL>
-__device__ __forceinline__ void stockham_t(cpx<T>* buf, const cpx<T>* st_tab, bool inverse,
-                                           bool lo_major) {
-  constexpr int TOT = 1 << (LN + LL);
-  constexpr int NST = (LN + 1) / 2;
+template <int LN>
+struct R8Plan {
+  static constexpr int n4 = (LN % 3 == 0) ? 0 : ((LN % 3 == 2) ? 1 : 2);
+  static constexpr int n8 = (LN - 2 * n4) / 3;
+  static constexpr int NST = n8 + n4;
+  __host__ __device__ static constexpr int lr(int s) { return s < n8 ? 3 : 2; }
+  __host__ __device__ static constexpr int lns(int s) {
+    return s <= n8 ? 3 * s : 3 * n8 + 2 * (s - n8);
+  }
+  __host__ __device__ static constexpr int toff(int s) {
+    int o = 0;
+    for (int i = 0; i < s; ++i) o += (1 << lns(i)) * ((1 << lr(i)) - 1);
+    return o;
+  }
+};
+
+__device__ __forceinline__ int fpad(int i) { return i + (i >> 4); }
+// padded tile slots for a 2048-point tile (+ the C2R staging overhang)
+constexpr int kFftTileSlots = 2048 + 2048 / 16 + 32;
+
+// per-stage twiddles of the radix-8/4 plan: stage s holds w^{jm r nt/(Ns R)}
+// at toff(s) + jm (R-1) + r-1
+template <typename T, int LN>
+__device__ void build_r8_twiddles(cpx<T>* st_tab, const cpx<T>* full, int full_step) {
+  using P = R8Plan<LN>;
 #pragma unroll
-  for (int s = 0; s < NST; ++s) {
-    const int lNs = 2 * s;
-    const int lR = (LN - lNs) >= 2 ? 2 : 1;
-    const int lg = LN - lR;
-    const int GPT = (TOT >> lR) / 256;  // groups per thread
-    const int toff = (1 << (2 * s)) - 1;  // sum over previous radix-4 stages of Ns * 3
+  for (int s = 0; s < P::NST; ++s) {
+    const int lR = P::lr(s), lNs = P::lns(s), R = 1 << lR;
+    const int tws = LN - lNs - lR;
+    for (int e = threadIdx.x; e < ((R - 1) << lNs); e += blockDim.x) {
+      const int jm = e / (R - 1), r = e % (R - 1) + 1;
+      st_tab[P::toff(s) + e] = full[((jm * r) << tws) * full_step];
+    }
+  }
+}
+
+// y *= exp(-+ 2 pi i m / 8) for m = 1, 2, 3 (INV: conjugate)
+template <typename T, bool INV, int M>
+__device__ __forceinline__ cpx<T> rot8(cpx<T> a) {
+  constexpr T h = (T)0.70710678118654752440;
+  if (M == 1) return INV ? cpx<T>{(a.re - a.im) * h, (a.re + a.im) * h}
+                         : cpx<T>{(a.re + a.im) * h, (a.im - a.re) * h};
+  if (M == 2) return INV ? cpx<T>{-a.im, a.re} : cpx<T>{a.im, -a.re};
+  return INV ? cpx<T>{(-a.re - a.im) * h, (a.re - a.im) * h}
+             : cpx<T>{(a.im - a.re) * h, (-a.re - a.im) * h};
+}
+
+// in-register DFT4 of x[o], x[o+s], x[o+2s], x[o+3s]; output k in place of input k
+template <typename T, bool INV>
+__device__ __forceinline__ void dft4(cpx<T>& x0, cpx<T>& x1, cpx<T>& x2, cpx<T>& x3) {
+  const cpx<T> c0 = cadd(x0, x2), c1 = csub(x0, x2), c2 = cadd(x1, x3);
+  const cpx<T> c3 = rot8<T, INV, 2>(csub(x1, x3));
+  x0 = cadd(c0, c2);
+  x2 = csub(c0, c2);
+  x1 = cadd(c1, c3);
+  x3 = csub(c1, c3);
+}
+
+// in-register DFT8 (decimation in frequency: X[2k] = DFT4(a), X[2k+1] = DFT4(b))
+template <typename T, bool INV>
+__device__ __forceinline__ void dft8(cpx<T>* x) {
+  cpx<T> a0 = cadd(x[0], x[4]), a1 = cadd(x[1], x[5]), a2 = cadd(x[2], x[6]), a3 = cadd(x[3], x[7]);
+  cpx<T> b0 = csub(x[0], x[4]);
+  cpx<T> b1 = rot8<T, INV, 1>(csub(x[1], x[5]));
+  cpx<T> b2 = rot8<T, INV, 2>(csub(x[2], x[6]));
+  cpx<T> b3 = rot8<T, INV, 3>(csub(x[3], x[7]));
+  dft4<T, INV>(a0, a1, a2, a3);
+  dft4<T, INV>(b0, b1, b2, b3);
+  x[0] = a0; x[2] = a1; x[4] = a2; x[6] = a3;
+  x[1] = b0; x[3] = b1; x[5] = b2; x[7] = b3;
+}
+
+template <typename T, int LN, int LL, bool INV>
+__device__ __forceinline__ void stockham8(cpx<T>* buf, const cpx<T>* st_tab, bool lo_major) {
+  using P = R8Plan<LN>;
+#pragma unroll
+  for (int s = 0; s < P::NST; ++s) {
+    const int lR = P::lr(s), lNs = P::lns(s), R = 1 << lR;
+    const int lg = LN - lR;  // log2 butterflies per line
     const int nsm = (1 << lNs) - 1;
-    cpx<T> v[4][4];
+    const int NB = 8 / R;    // butterflies per thread
+    cpx<T> v[8];
 #pragma unroll
-    for (int g = 0; g < GPT; ++g) {
+    for (int g = 0; g < NB; ++g) {
       const int e = threadIdx.x + g * 256;
       const int l = lo_major ? (e & ((1 << LL) - 1)) : (e >> lg);
-      const int j = lo_major ? (e >> LL) : (e & ((1 << lg) - 1));
-      const int jm = j & nsm;
+      const int b = lo_major ? (e >> LL) : (e & ((1 << lg) - 1));
+      const int jm = b & nsm;
 #pragma unroll
-      for (int r = 0; r < (1 << lR); ++r) {
-        const int k = j + (r << lg);
-        cpx<T> x = buf[lo_major ? (k << LL) + l : (l << LN) + k];
+      for (int r = 0; r < R; ++r) {
+        const int k = b + (r << lg);
+        cpx<T> x = buf[fpad(lo_major ? (k << LL) + l : (l << LN) + k)];
         if (r > 0 && s > 0) {
-          cpx<T> w = st_tab[toff + jm * ((1 << lR) - 1) + r - 1];
-          if (inverse) w.im = -w.im;
+          cpx<T> w = st_tab[P::toff(s) + jm * (R - 1) + r - 1];
+          if (INV) w.im = -w.im;
           x = cmulc(x, w);
         }
-        v[g][r] = x;
+        v[g * R + r] = x;
       }
+      if (R == 8) dft8<T, INV>(v);
+      else dft4<T, INV>(v[g * 4 + 0], v[g * 4 + 1], v[g * 4 + 2], v[g * 4 + 3]);
     }
     __syncthreads();
 #pragma unroll
-    for (int g = 0; g < GPT; ++g) {
+    for (int g = 0; g < NB; ++g) {
       const int e = threadIdx.x + g * 256;
       const int l = lo_major ? (e & ((1 << LL) - 1)) : (e >> lg);
-      const int j = lo_major ? (e >> LL) : (e & ((1 << lg) - 1));
-      const int base = ((j >> lNs) << (lNs + lR)) + (j & nsm);
-      auto at = [&](int r) -> cpx<T>& {
+      const int b = lo_major ? (e >> LL) : (e & ((1 << lg) - 1));
+      const int base = ((b >> lNs) << (lNs + lR)) + (b & nsm);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
         const int k = base + (r << lNs);
-        return buf[lo_major ? (k << LL) + l : (l << LN) + k];
-      };
-      if (lR == 2) {
-        const cpx<T> a0 = cadd(v[g][0], v[g][2]), a1 = csub(v[g][0], v[g][2]);
-        const cpx<T> a2 = cadd(v[g][1], v[g][3]);
-        const cpx<T> d = csub(v[g][1], v[g][3]);
-        const cpx<T> a3 = inverse ? cpx<T>{-d.im, d.re} : cpx<T>{d.im, -d.re};
-        at(0) = cadd(a0, a2);
-        at(1) = cadd(a1, a3);
-        at(2) = csub(a0, a2);
-        at(3) = csub(a1, a3);
-      } else {
-        at(0) = cadd(v[g][0], v[g][1]);
-        at(1) = csub(v[g][0], v[g][1]);
+        buf[fpad(lo_major ? (k << LL) + l : (l << LN) + k)] = v[g * R + r];
       }
     }
     __syncthreads();
@@ -843,13 +906,15 @@ __global__ void __launch_bounds__(256, 2) k_fft_t(const void* in, void* out,  //
   static_assert(TOT == 2048, "tile must hold 2048 points");
   extern __shared__ __align__(16) unsigned char fft_smem[];
   const int hn = n / 2;
-  const int bufc = L * (NT + 1);
+  constexpr int bufc = kFftTileSlots;
   const T osc = (T)out_scale;
   cpx<T>* ts = reinterpret_cast<cpx<T>*>(fft_smem);
   cpx<T>* const buf0 = ts + NT;
   __shared__ double denl[16];
   __shared__ int64_t lbase[16];
-  build_stage_twiddles<T>(ts, LN, tw, (mode == FFT_C2C) ? 1 : 2);
+  build_r8_twiddles<T, LN>(ts, tw, (mode == FFT_C2C) ? 1 : 2);
+  const bool inv_first = (mode == FFT_C2R) || inverse != 0;
+  constexpr int CS = (int)sizeof(cpx<T>);
   const bool lo_lines = st > 1;
   const int64_t nlob = lo_lines ? (st + L - 1) >> LL : 1;
   auto origin = [&](int64_t t, int64_t& lo0, int64_t& hi0) {
@@ -872,7 +937,12 @@ __global__ void __launch_bounds__(256, 2) k_fft_t(const void* in, void* out,  //
         const unsigned char* src =
             reinterpret_cast<const unsigned char*>(in) + hi0 * n * (int64_t)sizeof(T);
         const int64_t bytes = lines * n * (int64_t)sizeof(T);
-        for (int64_t o = tid * 16; o < bytes; o += 256 * 16) cpa16(sb + (uint32_t)o, src + o);
+        // one complex slot per copy: padded slots are only CS-byte aligned
+        for (int m = tid; m < (int)(bytes / CS); m += 256) {
+          const uint32_t d = sb + (uint32_t)(fpad(m) * CS);
+          if (CS == 8) cpa8(d, src + (int64_t)m * CS);
+          else cpa16(d, src + (int64_t)m * CS);
+        }
       } else if (mode == FFT_C2R) {
         // swapped layout (tr_n1) or plain; thread serves line l = tid mod L
         const cpx<T>* X = reinterpret_cast<const cpx<T>*>(in);
@@ -883,7 +953,7 @@ __global__ void __launch_bounds__(256, 2) k_fft_t(const void* in, void* out,  //
                                    : line * (hn + 1);
           const int64_t kst = tr_n1 ? tr_n1 : 1;
           for (int k = tid >> LL; k <= hn; k += 256 >> LL) {
-            const uint32_t d = sb + (uint32_t)((l * (hn + 1) + k) * (int)sizeof(cpx<T>));
+            const uint32_t d = sb + (uint32_t)(fpad(l * (hn + 1) + k) * CS);
             if (sizeof(cpx<T>) == 8) cpa8(d, X + gb + kst * k);
             else cpa16(d, X + gb + kst * k);
           }
@@ -898,7 +968,7 @@ __global__ void __launch_bounds__(256, 2) k_fft_t(const void* in, void* out,  //
 #pragma unroll
             for (int u = 0; u < PER; ++u) {
               const int k = (tid >> LL) + u * (256 >> LL);
-              const uint32_t d = sb + (uint32_t)(((k << LL) + l) * (int)sizeof(cpx<T>));
+              const uint32_t d = sb + (uint32_t)(fpad((k << LL) + l) * CS);
               if (sizeof(cpx<T>) == 8) cpa8(d, p + st * k);
               else cpa16(d, p + st * k);
             }
@@ -911,7 +981,7 @@ __global__ void __launch_bounds__(256, 2) k_fft_t(const void* in, void* out,  //
           for (int u = 0; u < PER; ++u) {
             const int e = tid + u * 256;
             if ((e >> LN) < lines) {
-              const uint32_t d = sb + (uint32_t)(e * (int)sizeof(cpx<T>));
+              const uint32_t d = sb + (uint32_t)(fpad(e) * CS);
               if (sizeof(cpx<T>) == 8) cpa8(d, p + e);
               else cpa16(d, p + e);
             }
@@ -952,7 +1022,7 @@ __global__ void __launch_bounds__(256, 2) k_fft_t(const void* in, void* out,  //
       for (int c = 0; c < PER; ++c) {
         const int e = tid + c * 256;
         const int l = e >> LN, k = e & (NT - 1);
-        const cpx<T> a = buf[l * (hn + 1) + k], bb = cconjt(buf[l * (hn + 1) + hn - k]);
+        const cpx<T> a = buf[fpad(l * (hn + 1) + k)], bb = cconjt(buf[fpad(l * (hn + 1) + hn - k)]);
         const cpx<T> E = {(a.re + bb.re) * T(0.5), (a.im + bb.im) * T(0.5)};
         cpx<T> w = tw[k];
         w.im = -w.im;
@@ -962,10 +1032,11 @@ __global__ void __launch_bounds__(256, 2) k_fft_t(const void* in, void* out,  //
       }
       __syncthreads();
 #pragma unroll
-      for (int c = 0; c < PER; ++c) buf[tid + c * 256] = zv[c];
+      for (int c = 0; c < PER; ++c) buf[fpad(tid + c * 256)] = zv[c];
       __syncthreads();
     }
-    stockham_t<T, LN, LL>(buf, ts, (mode == FFT_C2R) || inverse != 0, lo_lines);
+    if (inv_first) stockham8<T, LN, LL, true>(buf, ts, lo_lines);
+    else stockham8<T, LN, LL, false>(buf, ts, lo_lines);
     if (ss.active) {
       const int lo_off = ss.lam_off[ss.d - 1];
 #pragma unroll
@@ -975,11 +1046,11 @@ __global__ void __launch_bounds__(256, 2) k_fft_t(const void* in, void* out,  //
         const int k = lo_lines ? (e >> LL) : (e & (NT - 1));
         const double den = denl[l] + (lo_off >= 0 ? lam[lo_off + k] : 0.0);
         const T inv = (T)(1.0 / den);
-        const cpx<T> v = buf[e];
-        buf[e] = {v.re * inv, v.im * inv};
+        const cpx<T> v = buf[fpad(e)];
+        buf[fpad(e)] = {v.re * inv, v.im * inv};
       }
       __syncthreads();
-      stockham_t<T, LN, LL>(buf, ts, true, lo_lines);
+      stockham8<T, LN, LL, true>(buf, ts, lo_lines);
     }
     if (mode == FFT_R2C) {
       cpx<T>* Xo = reinterpret_cast<cpx<T>*>(out);
@@ -987,8 +1058,8 @@ __global__ void __launch_bounds__(256, 2) k_fft_t(const void* in, void* out,  //
       const int l = tid & (L - 1);
       if (hi0 + l < hi) {
         for (int k = tid >> LL; k <= hn; k += 256 >> LL) {
-          const cpx<T> a = buf[(l << LN) + (k & (NT - 1))];
-          const cpx<T> bb = cconjt(buf[(l << LN) + ((NT - k) & (NT - 1))]);
+          const cpx<T> a = buf[fpad((l << LN) + (k & (NT - 1)))];
+          const cpx<T> bb = cconjt(buf[fpad((l << LN) + ((NT - k) & (NT - 1)))]);
           const cpx<T> E = {(a.re + bb.re) * T(0.5), (a.im + bb.im) * T(0.5)};
           const cpx<T> D = {(a.re - bb.re) * T(0.5), (a.im - bb.im) * T(0.5)};
           const cpx<T> O = {D.im, -D.re};
@@ -1002,7 +1073,7 @@ __global__ void __launch_bounds__(256, 2) k_fft_t(const void* in, void* out,  //
         const int l = e >> LN, k = e & (NT - 1);
         const int64_t line = hi0 + l;
         if (line < hi) {
-          const cpx<T> v = buf[e];
+          const cpx<T> v = buf[fpad(e)];
           reinterpret_cast<cpx<T>*>(out)[line * NT + k] = {v.re * osc, v.im * osc};  // x[2k], x[2k+1]
         }
       }
@@ -1013,7 +1084,7 @@ __global__ void __launch_bounds__(256, 2) k_fft_t(const void* in, void* out,  //
 #pragma unroll
         for (int u = 0; u < PER; ++u) {
           const int k = (tid >> LL) + u * (256 >> LL);
-          const cpx<T> v = buf[(k << LL) + l];
+          const cpx<T> v = buf[fpad((k << LL) + l)];
           p[st * k] = {v.re * osc, v.im * osc};
         }
       }
@@ -1023,7 +1094,7 @@ __global__ void __launch_bounds__(256, 2) k_fft_t(const void* in, void* out,  //
 #pragma unroll
       for (int u = 0; u < PER; ++u) {
         const int e = tid + u * 256;
-        const cpx<T> v = buf[e];
+        const cpx<T> v = buf[fpad(e)];
         if ((e >> LN) < lines) p[e] = {v.re * osc, v.im * osc};
       }
     }

@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kPjThreads, 1)
   __shared__ float wtile[128][33];
   unsigned char* smem = (unsigned char*)(((uintptr_t)pj_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = smem_u32(smem);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = tid >> 5;
   const int64_t ntiles = (n + 127) / 128;
   const int kt = (int)(m / 32);
   const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
