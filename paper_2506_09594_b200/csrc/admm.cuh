@@ -9,6 +9,7 @@
 // own stream with its own workspace, so the modes overlap on the GPU.
 #pragma once
 
+#include <initializer_list>
 #include <limits>
 #include <vector>
 
@@ -380,6 +381,64 @@ enum {
   R_Y_NORM, R_LAG_NORM, R_MU, R_REL_DL, R_BOX_GAP, R_NOUT
 };
 
+// 16-byte vector path of the line kernels: axis 0 a multiple of 4 and every
+// buffer 16-byte aligned (the mask 4-byte aligned)
+template <typename T>
+static bool line_vec4(const Geom& g, std::initializer_list<const void*> ptrs,
+                      const void* mask = nullptr) {
+  if (g.dims[0] % 4 != 0) return false;
+  for (const void* p : ptrs)
+    if (p && ((uintptr_t)p & 15)) return false;
+  return !mask || ((uintptr_t)mask & 3) == 0;
+}
+
+// multiplier updates of modes [0, nm) in groups of up to 4 (one pass over the
+// iterate per group), each group's residuals reduced into res + 5 k0
+template <typename T>
+static void lag_updates(Solver<T>& s, const T* x, double mu, bool v4, unsigned grid,
+                        cudaStream_t st) {
+  const int nm = s.cfg.nmodes;
+  for (int k0 = 0; k0 < nm; k0 += 4) {
+    const int cnt = std::min(4, nm - k0);
+    ModePtrs<T> gn{}, go{}, lg{};
+    gn.count = go.count = lg.count = cnt;
+    for (int k = 0; k < cnt; ++k) {
+      gn.p[k] = s.gnew[k0 + k];
+      go.p[k] = s.gcur[k0 + k];
+      lg.p[k] = s.lag[k0 + k];
+      gn.axis[k] = go.axis[k] = lg.axis[k] = s.cfg.modes[k0 + k];
+    }
+#define TR_LU(NM)                                                                               \
+  launch("lag_update", v4 ? k_lag_update<T, 4, NM> : k_lag_update<T, 1, NM>, grid, kRedThreads, \
+         0, st, s.g, x, gn, go, lg, mu, s.part)
+    switch (cnt) {
+      case 1: TR_LU(1); break;
+      case 2: TR_LU(2); break;
+      case 3: TR_LU(3); break;
+      default: TR_LU(4); break;
+    }
+#undef TR_LU
+    unsigned mask = 0;
+    for (int k = 0; k < cnt; ++k) mask |= 0b00101u << (5 * k);
+    launch("final_reduce", k_final_reduce, 1, 256, 0, st, (const double*)s.part, (int)grid,
+           5 * cnt, mask, s.res + 5 * k0);
+  }
+}
+
+template <typename T>
+static void lrta_inputs(Solver<T>& s, const T* x, double mu, bool v4, unsigned grid,
+                        cudaStream_t st) {
+  ModePtrs<T> lg{}, xs{};
+  lg.count = xs.count = s.cfg.nmodes;
+  for (int k = 0; k < s.cfg.nmodes; ++k) {
+    lg.p[k] = s.lag[k];
+    xs.p[k] = s.X[k];
+    lg.axis[k] = xs.axis[k] = s.cfg.modes[k];
+  }
+  launch("lrta_input", v4 ? k_lrta_input<T, 4> : k_lrta_input<T, 1>, grid, kRedThreads, 0, st,
+         s.g, x, lg, xs, mu);
+}
+
 template <typename T>
 static int admm_step(Solver<T>& s, double* hout) {
   cudaStream_t st = s.streams[0];
@@ -397,6 +456,8 @@ static int admm_step(Solver<T>& s, double* hout) {
     lp.p[k] = s.lag[k];
   }
   const bool pure = nm == 1 && s.cfg.modes[0] < 0;
+  const bool v4 = line_vec4<T>(g, {s.A, s.B, s.l, s.e, s.y, s.z, s.lold, s.rhs}, s.mask);
+  const auto rhs_k = v4 ? k_admm_rhs<T, 4> : k_admm_rhs<T, 1>;
   double* part = s.part;
   double* res = s.res;  // device scratch for final reductions
   const int64_t rb = grid;
@@ -405,24 +466,15 @@ static int admm_step(Solver<T>& s, double* hout) {
   if (!s.onebit()) {
     // L-subproblem (solvers.py:231-233)
     if (pure) {
-      launch("admm_rhs", k_admm_rhs<T>, grid, kRedThreads, 0, st, g, s.A, s.e, s.y, mu, gp, lp,
-             s.l);
+      launch("admm_rhs", rhs_k, grid, kRedThreads, 0, st, g, s.A, s.e, s.y, mu, gp, lp, s.l);
     } else {
-      launch("admm_rhs", k_admm_rhs<T>, grid, kRedThreads, 0, st, g, s.A, s.e, s.y, mu, gp, lp,
-             s.rhs);
+      launch("admm_rhs", rhs_k, grid, kRedThreads, 0, st, g, s.A, s.e, s.y, mu, gp, lp, s.rhs);
       if (fft_solve2<T>(s, s.rhs, s.l, st)) return 1;
     }
     tau = 1.0 / (gamma * mu);
-    for (int k = 0; k < nm; ++k)
-      launch("lrta_input", k_lrta_input<T>, grid, kRedThreads, 0, st, g, (const T*)s.l,
-             s.cfg.modes[k], (const T*)s.lag[k], mu, s.X[k]);
+    lrta_inputs<T>(s, s.l, mu, v4, grid, st);
     if (low_rank_step<T>(s, tau)) return 2;
-    for (int k = 0; k < nm; ++k) {
-      launch("lag_update", k_lag_update<T>, grid, kRedThreads, 0, st, g, (const T*)s.l,
-             s.cfg.modes[k], (const T*)s.gnew[k], (const T*)s.gcur[k], s.lag[k], mu, part);
-      launch("final_reduce", k_final_reduce, 1, 256, 0, st, (const double*)part, (int)rb, 5,
-             0b00101u, res + 5 * k);
-    }
+    lag_updates<T>(s, s.l, mu, v4, grid, st);
     // noise and dual updates (solvers.py:239-246)
     const double level = s.cfg.lam / mu;
     const int structure = s.cfg.kind == 1 ? 3 : s.cfg.structure;
@@ -437,7 +489,8 @@ static int admm_step(Solver<T>& s, double* hout) {
 #undef TR_GS
     }
 #define TR_ND2(K, S)                                                                          \
-  launch("noise_dual", k_noise_dual<T, K, S>, grid, kRedThreads, 0, st, g, s.A, s.mask,      \
+  launch("noise_dual", v4 ? k_noise_dual<T, K, S, 4> : k_noise_dual<T, K, S, 1>, grid,        \
+         kRedThreads, 0, st, g, s.A, s.mask,                                                   \
          (const T*)s.l, (const T*)s.lold, s.e, s.y, mu, q0, q1, level, (const double*)s.scale, \
          part)
 #define TR_ND(K)                            \
@@ -466,28 +519,21 @@ static int admm_step(Solver<T>& s, double* hout) {
            res + 80);
     // Z-subproblem: solve with b = L + Y / mu
     if (pure) {
-      launch("admm_rhs", k_admm_rhs<T>, grid, kRedThreads, 0, st, g, (const T*)s.l, (const T*)nullptr,
+      launch("admm_rhs", rhs_k, grid, kRedThreads, 0, st, g, (const T*)s.l, (const T*)nullptr,
              s.y, mu, gp, lp, s.z);
     } else {
-      launch("admm_rhs", k_admm_rhs<T>, grid, kRedThreads, 0, st, g, (const T*)s.l, (const T*)nullptr,
+      launch("admm_rhs", rhs_k, grid, kRedThreads, 0, st, g, (const T*)s.l, (const T*)nullptr,
              s.y, mu, gp, lp, s.rhs);
       if (fft_solve2<T>(s, s.rhs, s.z, st)) return 1;
     }
     tau = s.cfg.lam / (gamma * mu);
-    for (int k = 0; k < nm; ++k)
-      launch("lrta_input", k_lrta_input<T>, grid, kRedThreads, 0, st, g, (const T*)s.z,
-             s.cfg.modes[k], (const T*)s.lag[k], mu, s.X[k]);
+    lrta_inputs<T>(s, s.z, mu, v4, grid, st);
     if (low_rank_step<T>(s, tau)) return 2;
     launch("onebit_dual", k_onebit_dual<T>, grid, kRedThreads, 0, st, N, (const T*)s.l,
            (const T*)s.z, s.y, mu, part);
     launch("final_reduce", k_final_reduce, 1, 256, 0, st, (const double*)part, (int)rb, 2, 0b01u,
            res + 90);
-    for (int k = 0; k < nm; ++k) {
-      launch("lag_update", k_lag_update<T>, grid, kRedThreads, 0, st, g, (const T*)s.z,
-             s.cfg.modes[k], (const T*)s.gnew[k], (const T*)s.gcur[k], s.lag[k], mu, part);
-      launch("final_reduce", k_final_reduce, 1, 256, 0, st, (const double*)part, (int)rb, 5,
-             0b00101u, res + 5 * k);
-    }
+    lag_updates<T>(s, s.z, mu, v4, grid, st);
   }
   TR_LAUNCH_CHECK();
   TR_CUDA(cudaMemcpyAsync(s.hres, res, 128 * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -600,7 +646,7 @@ static int admm_create(const AdmmConfig& cfg, int order, const int64_t* dims, co
   s->lam = s->template alloc<double>(lam_total);
   s->scale = s->template alloc<double>(std::max<int64_t>(dims[0] * dims[1], N / (dims[0] * dims[1])));
   s->red_blocks = grid_for<T>(N);
-  s->part = s->template alloc<double>(s->red_blocks * 8);
+  s->part = s->template alloc<double>(s->red_blocks * 20);  // up to 4 modes x 5 partials
   s->res = s->template alloc<double>(128);
   for (void* p : s->allocs)
     if (!p) {
@@ -733,8 +779,10 @@ static int gradsys_solve(Solver<T>& s, const T* b, const T* const* grads, T* out
     gm.axis[k] = lag.axis[k] = s.cfg.modes[k];
   }
   const double inf = std::numeric_limits<double>::infinity();
-  launch("admm_rhs", k_admm_rhs<T>, (unsigned)grid_for<T>(s.g.N), kRedThreads, 0, st, s.g, b,
-         (const T*)nullptr, b, inf, gm, lag, s.rhs);
+  bool v4 = line_vec4<T>(s.g, {b, out, s.rhs});
+  for (int k = 0; k < s.cfg.nmodes; ++k) v4 = v4 && ((uintptr_t)grads[k] & 15) == 0;
+  launch("admm_rhs", v4 ? k_admm_rhs<T, 4> : k_admm_rhs<T, 1>, (unsigned)grid_for<T>(s.g.N),
+         kRedThreads, 0, st, s.g, b, (const T*)nullptr, b, inf, gm, lag, s.rhs);
   return fft_solve2<T>(s, s.rhs, out, st);
 }
 

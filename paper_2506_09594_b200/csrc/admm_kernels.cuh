@@ -50,6 +50,98 @@ struct ModePtrs {
   T* p[kMaxOrder];
 };
 
+// V consecutive elements of one line (V = 4: 16-byte accesses when the host
+// checked n0 % 4 == 0 and 16-byte aligned buffers; V = 1 otherwise).
+template <typename T, int V>
+struct Vec {
+  T x[V];
+};
+
+template <typename T, int V>
+__device__ __forceinline__ Vec<T, V> ldv(const T* p) {
+  Vec<T, V> r;
+  if constexpr (V == 4 && sizeof(T) == 4) {
+    const float4 f = *reinterpret_cast<const float4*>(p);
+    r.x[0] = f.x; r.x[1] = f.y; r.x[2] = f.z; r.x[3] = f.w;
+  } else if constexpr (V == 4 && sizeof(T) == 8) {
+    const double2 a = reinterpret_cast<const double2*>(p)[0];
+    const double2 b = reinterpret_cast<const double2*>(p)[1];
+    r.x[0] = a.x; r.x[1] = a.y; r.x[2] = b.x; r.x[3] = b.y;
+  } else {
+#pragma unroll
+    for (int j = 0; j < V; ++j) r.x[j] = p[j];
+  }
+  return r;
+}
+
+template <typename T, int V>
+__device__ __forceinline__ void stv(T* p, const T (&v)[V]) {
+  if constexpr (V == 4 && sizeof(T) == 4) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  } else if constexpr (V == 4 && sizeof(T) == 8) {
+    reinterpret_cast<double2*>(p)[0] = make_double2(v[0], v[1]);
+    reinterpret_cast<double2*>(p)[1] = make_double2(v[2], v[3]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < V; ++j) p[j] = v[j];
+  }
+}
+
+template <int V>
+__device__ __forceinline__ void ld_mask(const uint8_t* p, bool (&m)[V]) {
+  if constexpr (V == 4) {
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(p);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) m[j] = ((w >> (8 * j)) & 0xffu) != 0;
+  } else {
+#pragma unroll
+    for (int j = 0; j < V; ++j) m[j] = p[j] != 0;
+  }
+}
+
+// Walk every V-element chunk of every axis-0 line: f(line, i0).  Long lines
+// are split across the block's threads; short lines pack several per pass.
+template <int V, typename F>
+__device__ __forceinline__ void for_each_chunk(const Geom& g, F&& f) {
+  const int64_t n0 = g.dims[0], lines = g.N / n0;
+  const int cpl = (int)(n0 / V);
+  if (cpl >= (int)blockDim.x) {
+    for (int64_t line = blockIdx.x; line < lines; line += gridDim.x)
+      for (int c = threadIdx.x; c < cpl; c += blockDim.x) f(line, (int64_t)c * V);
+  } else {
+    const int lpi = (int)blockDim.x / cpl;
+    const int sub = (int)threadIdx.x / cpl, c = (int)threadIdx.x - sub * cpl;
+    if (sub >= lpi) return;
+    for (int64_t l0 = (int64_t)blockIdx.x * lpi; l0 < lines; l0 += (int64_t)gridDim.x * lpi) {
+      const int64_t line = l0 + sub;
+      if (line < lines) f(line, (int64_t)c * V);
+    }
+  }
+}
+
+// forward difference D_a x at the V elements of a chunk (x already loaded);
+// a < 0: identity chain
+template <typename T, int V>
+__device__ __forceinline__ void fwd_diff(const Geom& g, const T* x, int a, int64_t line,
+                                         int64_t base, int64_t i0, const Vec<T, V>& xv,
+                                         T (&out)[V]) {
+  const int64_t n0 = g.dims[0];
+  if (a < 0) {
+#pragma unroll
+    for (int j = 0; j < V; ++j) out[j] = xv.x[j];
+  } else if (a == 0) {
+    const T last = x[base + (i0 + V < n0 ? i0 + V : 0)];
+#pragma unroll
+    for (int j = 0; j < V; ++j) out[j] = (j + 1 < V ? xv.x[j + 1] : last) - xv.x[j];
+  } else {
+    int64_t pv, nx;
+    axis_offsets(g, a, line_coord(g, line, a), pv, nx);
+    const Vec<T, V> xn = ldv<T, V>(x + base + i0 + nx);
+#pragma unroll
+    for (int j = 0; j < V; ++j) out[j] = xn.x[j] - xv.x[j];
+  }
+}
+
 template <int KIND>
 __device__ __forceinline__ double prox_k(double p0, double p1, double mu, double v) {
   Penalty pen{KIND, p0, p1};
@@ -84,107 +176,127 @@ __global__ void k_final_reduce(const double* __restrict__ part, int nblocks, int
 // rhs of the L- (or Z-) subproblem (solvers.py:231-233, onebit.py:182-184):
 //   b = A - B + y / mu ;  rhs = b + sum_k D_k^T (g_k - lag_k / mu)
 // pure low-rank chain: out = 0.5 * (b + g - lag / mu)  (solvers.py:194-195), the final L.
-template <typename T>
+template <typename T, int V>
 __global__ void __launch_bounds__(kRedThreads) k_admm_rhs(Geom g, const T* __restrict__ A,
                                                           const T* __restrict__ B,
                                                           const T* __restrict__ y, double mu,
                                                           ModePtrs<T> gm, ModePtrs<T> lag,
                                                           T* __restrict__ out) {
-  const int64_t n0 = g.dims[0], lines = g.N / n0;
+  const int64_t n0 = g.dims[0];
   const T imu = (T)(1.0 / mu);
   const bool pure = gm.count == 1 && gm.axis[0] < 0;
-  for (int64_t line = blockIdx.x; line < lines; line += gridDim.x) {
-    int64_t prevoff[kMaxOrder];
+  for_each_chunk<V>(g, [&](int64_t line, int64_t i0) {
+    const int64_t base = line * n0, i = base + i0;
+    const Vec<T, V> av = ldv<T, V>(A + i), yv = ldv<T, V>(y + i);
+    Vec<T, V> bv;
+    if (B) bv = ldv<T, V>(B + i);
+    T acc[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) acc[j] = (B ? (av.x[j] - bv.x[j]) : av.x[j]) + yv.x[j] * imu;
+    if (pure) {
+      const Vec<T, V> gv = ldv<T, V>(gm.p[0] + i), lv = ldv<T, V>(lag.p[0] + i);
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc[j] = (T)0.5 * (acc[j] + (gv.x[j] - lv.x[j] * imu));
+      stv<T, V>(out + i, acc);
+      return;
+    }
 #pragma unroll
     for (int k = 0; k < kMaxOrder; ++k) {
-      prevoff[k] = 0;
-      if (k < gm.count && gm.axis[k] > 0) {
-        int64_t nx;
-        axis_offsets(g, gm.axis[k], line_coord(g, line, gm.axis[k]), prevoff[k], nx);
-      }
-    }
-    const int64_t base = line * n0;
-    for (int64_t i0 = threadIdx.x; i0 < n0; i0 += blockDim.x) {
-      const int64_t i = base + i0;
-      const T bv = (B ? (A[i] - B[i]) : A[i]) + y[i] * imu;
-      if (pure) {
-        out[i] = (T)0.5 * (bv + (gm.p[0][i] - lag.p[0][i] * imu));
-        continue;
-      }
-      T acc = bv;
+      if (k < gm.count) {
+        const int a = gm.axis[k];
+        const Vec<T, V> gv = ldv<T, V>(gm.p[k] + i), lv = ldv<T, V>(lag.p[k] + i);
+        T gi[V], gp[V];
 #pragma unroll
-      for (int k = 0; k < kMaxOrder; ++k) {
-        if (k < gm.count) {
-          const int a = gm.axis[k];
-          const int64_t ip = a == 0 ? base + (i0 > 0 ? i0 - 1 : n0 - 1) : i + prevoff[k];
-          const T gi = gm.p[k][i] - lag.p[k][i] * imu;
-          const T gp = gm.p[k][ip] - lag.p[k][ip] * imu;
-          acc += gp - gi;
+        for (int j = 0; j < V; ++j) gi[j] = gv.x[j] - lv.x[j] * imu;
+        if (a == 0) {
+          const int64_t ip = base + (i0 > 0 ? i0 - 1 : n0 - 1);
+          gp[0] = gm.p[k][ip] - lag.p[k][ip] * imu;
+#pragma unroll
+          for (int j = 1; j < V; ++j) gp[j] = gi[j - 1];
+        } else {
+          int64_t pv, nx;
+          axis_offsets(g, a, line_coord(g, line, a), pv, nx);
+          const Vec<T, V> gq = ldv<T, V>(gm.p[k] + i + pv), lq = ldv<T, V>(lag.p[k] + i + pv);
+#pragma unroll
+          for (int j = 0; j < V; ++j) gp[j] = gq.x[j] - lq.x[j] * imu;
         }
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[j] += gp[j] - gi[j];
       }
-      out[i] = acc;
     }
-  }
-  (void)imu;
+    stv<T, V>(out + i, acc);
+  });
 }
 
-// LRTA input of mode `axis`: X = D_axis L + lag / mu (identity chain: L + lag / mu)
-template <typename T>
+// LRTA inputs of every mode (one pass over L): X_k = D_k L + lag_k / mu
+// (identity chain: L + lag / mu)
+template <typename T, int V>
 __global__ void __launch_bounds__(kRedThreads) k_lrta_input(Geom g, const T* __restrict__ l,
-                                                            int axis, const T* __restrict__ lag,
-                                                            double mu, T* __restrict__ X) {
+                                                            ModePtrs<T> lag, ModePtrs<T> X,
+                                                            double mu) {
   const T imu = (T)(1.0 / mu);
-  const int64_t n0 = g.dims[0], lines = g.N / n0;
-  for (int64_t line = blockIdx.x; line < lines; line += gridDim.x) {
-    int64_t pv = 0, nx = 0;
-    if (axis > 0) axis_offsets(g, axis, line_coord(g, line, axis), pv, nx);
-    const int64_t base = line * n0;
-    for (int64_t i0 = threadIdx.x; i0 < n0; i0 += blockDim.x) {
-      const int64_t i = base + i0;
-      T gl;
-      if (axis < 0) gl = l[i];
-      else if (axis == 0) gl = l[base + (i0 + 1 < n0 ? i0 + 1 : 0)] - l[i];
-      else gl = l[i + nx] - l[i];
-      X[i] = gl + lag[i] * imu;
+  const int64_t n0 = g.dims[0];
+  for_each_chunk<V>(g, [&](int64_t line, int64_t i0) {
+    const int64_t base = line * n0, i = base + i0;
+    const Vec<T, V> lv = ldv<T, V>(l + i);
+#pragma unroll
+    for (int k = 0; k < kMaxOrder; ++k) {
+      if (k < lag.count) {
+        T gl[V];
+        fwd_diff<T, V>(g, l, lag.axis[k], line, base, i0, lv, gl);
+        const Vec<T, V> mv = ldv<T, V>(lag.p[k] + i);
+        T o[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) o[j] = gl[j] + mv.x[j] * imu;
+        stv<T, V>(X.p[k] + i, o);
+      }
     }
-  }
+  });
 }
 
-// multiplier update of one mode (solvers.py:247-248) with its residuals:
-//   lag += mu (D L - G_new);  partial q: 0 max|DL-G|, 1 sum (DL-G)^2,
+// multiplier updates of NM modes (solvers.py:247-248) with their residuals:
+//   lag_k += mu (D_k L - G_new,k);  partial 5k+q: 0 max|DL-G|, 1 sum (DL-G)^2,
 //   2 max|G_new-G_old|, 3 sum (G_new-G_old)^2, 4 sum lag_new^2
-template <typename T>
-__global__ void __launch_bounds__(kRedThreads) k_lag_update(Geom g, const T* __restrict__ l, int axis,
-                                                            const T* __restrict__ gnew,
-                                                            const T* __restrict__ gold,
-                                                            T* __restrict__ lag, double mu,
+template <typename T, int V, int NM>
+__global__ void __launch_bounds__(kRedThreads) k_lag_update(Geom g, const T* __restrict__ l,
+                                                            ModePtrs<T> gnew, ModePtrs<T> gold,
+                                                            ModePtrs<T> lag, double mu,
                                                             double* __restrict__ part) {
   __shared__ double red[32];
-  double v[5] = {0, 0, 0, 0, 0};
-  const int64_t n0 = g.dims[0], lines = g.N / n0;
-  for (int64_t line = blockIdx.x; line < lines; line += gridDim.x) {
-    int64_t pv = 0, nx = 0;
-    if (axis > 0) axis_offsets(g, axis, line_coord(g, line, axis), pv, nx);
-    const int64_t base = line * n0;
-    for (int64_t i0 = threadIdx.x; i0 < n0; i0 += blockDim.x) {
-      const int64_t i = base + i0;
-      T gl;
-      if (axis < 0) gl = l[i];
-      else if (axis == 0) gl = l[base + (i0 + 1 < n0 ? i0 + 1 : 0)] - l[i];
-      else gl = l[i + nx] - l[i];
-      const T gn = gnew[i];
-      const T gap = gl - gn;
-      const T ln = lag[i] + (T)mu * gap;
-      lag[i] = ln;
-      const double dg = (double)gn - (double)gold[i];
-      v[0] = fmax(v[0], fabs((double)gap));
-      v[1] += (double)gap * (double)gap;
-      v[2] = fmax(v[2], fabs(dg));
-      v[3] += dg * dg;
-      v[4] += (double)ln * (double)ln;
+  double v[5 * NM];
+#pragma unroll
+  for (int q = 0; q < 5 * NM; ++q) v[q] = 0.0;
+  const int64_t n0 = g.dims[0];
+  const T tmu = (T)mu;
+  for_each_chunk<V>(g, [&](int64_t line, int64_t i0) {
+    const int64_t base = line * n0, i = base + i0;
+    const Vec<T, V> lv = ldv<T, V>(l + i);
+#pragma unroll
+    for (int k = 0; k < NM; ++k) {
+      T gl[V];
+      fwd_diff<T, V>(g, l, lag.axis[k], line, base, i0, lv, gl);
+      const Vec<T, V> gn = ldv<T, V>(gnew.p[k] + i), go = ldv<T, V>(gold.p[k] + i);
+      const Vec<T, V> lo = ldv<T, V>(lag.p[k] + i);
+      T ln[V];
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const T gap = gl[j] - gn.x[j];
+        ln[j] = lo.x[j] + tmu * gap;
+        const double dg = (double)gn.x[j] - (double)go.x[j];
+        v[5 * k + 0] = fmax(v[5 * k + 0], fabs((double)gap));
+        v[5 * k + 1] += (double)gap * (double)gap;
+        v[5 * k + 2] = fmax(v[5 * k + 2], fabs(dg));
+        v[5 * k + 3] += dg * dg;
+        v[5 * k + 4] += (double)ln[j] * (double)ln[j];
+      }
+      stv<T, V>(lag.p[k] + i, ln);
     }
-  }
-  block_partials<5>(v, 0b00101u, red, part);
+  });
+  constexpr unsigned kMaxMask = 0b00101u;
+  unsigned mask = 0;
+#pragma unroll
+  for (int k = 0; k < NM; ++k) mask |= kMaxMask << (5 * k);
+  block_partials<5 * NM>(v, mask, red, part);
 }
 
 // group scales of the structured noise shrinkage (shrink.py:49-54) of
@@ -250,7 +362,7 @@ __device__ __forceinline__ T prox_t(T p0, double p0d, double p1d, T mu, double m
 }
 
 // STRUCT: 0 entry, 1 tube, 2 slice, 3 noise-free (E = 0 on the mask)
-template <typename T, int KIND, int STRUCT>
+template <typename T, int KIND, int STRUCT, int V>
 __global__ void __launch_bounds__(kRedThreads) k_noise_dual(Geom g, const T* __restrict__ mobs,
                                                             const uint8_t* __restrict__ mask,
                                                             const T* __restrict__ l,
@@ -264,36 +376,45 @@ __global__ void __launch_bounds__(kRedThreads) k_noise_dual(Geom g, const T* __r
   // per-thread partials in T (fp32 sums over <= a few hundred elements), per-block fp64
   T v[7] = {T(0), T(0), T(0), T(0), T(0), T(0), T(0)};
   const int64_t face = g.dims[0] * g.dims[1];
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t n0 = g.dims[0];
   const T tmu = (T)mu, tlev = (T)level, tp0 = (T)p0, timu = (T)(1.0 / mu);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.N; i += stride) {
-    const T mi = mobs[i], li = l[i], yi = y[i], eo = e[i], lo = lold[i];
-    const bool obs = mask[i] != 0;
-    const T h = mi - li + yi * timu;
-    T en;
-    if (!obs) {
-      en = h;
-    } else if (STRUCT == 3) {
-      en = T(0);
-    } else if (STRUCT == 0) {
-      en = prox_t<KIND, T>(tp0, p0, p1, tlev, level, h);
-    } else {
-      const double sc = STRUCT == 1 ? scale[i % face] : scale[i / face];
-      en = (T)((double)h * sc);
+  for_each_chunk<V>(g, [&](int64_t line, int64_t i0) {
+    const int64_t i = line * n0 + i0;
+    const Vec<T, V> mv = ldv<T, V>(mobs + i), lv = ldv<T, V>(l + i), yv = ldv<T, V>(y + i);
+    const Vec<T, V> ev = ldv<T, V>(e + i), ov = ldv<T, V>(lold + i);
+    bool obs[V];
+    ld_mask<V>(mask + i, obs);
+    T en[V], yn[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const T mi = mv.x[j], li = lv.x[j], yi = yv.x[j];
+      const T h = mi - li + yi * timu;
+      T ej;
+      if (!obs[j]) {
+        ej = h;
+      } else if (STRUCT == 3) {
+        ej = T(0);
+      } else if (STRUCT == 0) {
+        ej = prox_t<KIND, T>(tp0, p0, p1, tlev, level, h);
+      } else {
+        const double sc = STRUCT == 1 ? scale[(i + j) % face] : scale[(i + j) / face];
+        ej = (T)((double)h * sc);
+      }
+      const T fit = mi - li - ej;
+      en[j] = ej;
+      yn[j] = yi + tmu * fit;
+      const T dl = li - ov.x[j], de = ej - ev.x[j];
+      v[0] = fmax(v[0], fabs(dl));
+      v[1] += dl * dl;
+      v[2] = fmax(v[2], fabs(de));
+      v[3] += de * de;
+      v[4] = fmax(v[4], fabs(fit));
+      v[5] += fit * fit;
+      v[6] += yn[j] * yn[j];
     }
-    const T fit = mi - li - en;
-    const T yn = yi + tmu * fit;
-    e[i] = en;
-    y[i] = yn;
-    const T dl = li - lo, de = en - eo;
-    v[0] = fmax(v[0], fabs(dl));
-    v[1] += dl * dl;
-    v[2] = fmax(v[2], fabs(de));
-    v[3] += de * de;
-    v[4] = fmax(v[4], fabs(fit));
-    v[5] += fit * fit;
-    v[6] += yn * yn;
-  }
+    stv<T, V>(e + i, en);
+    stv<T, V>(y + i, yn);
+  });
   double vd[7];
 #pragma unroll
   for (int q = 0; q < 7; ++q) vd[q] = (double)v[q];
