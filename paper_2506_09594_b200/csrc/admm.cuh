@@ -356,9 +356,11 @@ static int full_svt(Solver<T>& s, const T* X, T* out, double tau, void* ws, cuda
 template <typename T>
 static int low_rank_step(Solver<T>& s, double tau) {
   // fork: each mode on its own stream after the main stream's LRTA inputs
+  // (TR_SERIAL_MODES: all on the main stream, for uncontended kernel timings)
+  static const bool serial = getenv("TR_SERIAL_MODES") != nullptr;
   TR_CUDA(cudaEventRecord(s.ev_main, s.streams[0]));
   for (int k = 0; k < s.cfg.nmodes; ++k) {
-    cudaStream_t sk = s.streams[k + 1];
+    cudaStream_t sk = serial ? s.streams[0] : s.streams[k + 1];
     TR_CUDA(cudaStreamWaitEvent(sk, s.ev_main, 0));
     int rc;
     if (s.cfg.randomized)

@@ -393,15 +393,6 @@ __global__ void __launch_bounds__(256) k_fft_axis(const void* in, void* out,  //
   }
 }
 
-__device__ __forceinline__ void cpa8(uint32_t dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cpa16(uint32_t dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cpa_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-
 // Persistent, double-buffered variant for power-of-two transform lengths:
 // while tile t is transformed in one buffer, tile t+1 streams into the other
 // (cp.async), so HBM stays busy through the butterflies.  Same modes and

@@ -345,7 +345,7 @@ static int bki_mode(const T* A, int64_t m, int64_t n, int r, int b, int q, Sketc
     }
     launch("ritz", k_ritz_warp<T>, 1, 256, sm, st, bf.M, s, bf.Z, m, r, V, F, Ft, info);
   } else {
-    launch("ritz", k_ritz<T>, 1, 512, 2 * 64 * 65 * sizeof(double), st, bf.M, s, bf.Z, m, r, V,
+    launch("ritz", k_ritz<T>, 1, 256, 2 * 64 * 65 * sizeof(double), st, bf.M, s, bf.Z, m, r, V,
            F, Ft, info);
   }
   TR_LAUNCH_CHECK();
@@ -462,15 +462,21 @@ static int expand(const Shape& sh, Bufs<T>& bf, T* out, cudaStream_t st) {
   const int64_t N = sh.n2 * sh.nf;
   launch("expand_mode1", k_expand_mode1<T>, (unsigned)cdiv(sh.r0 * N, 256), 256, 0, st, 
       bf.core, (int)sh.r0, (int)sh.r1, sh.nf, bf.F1, sh.n2, bf.C1);
-  dim3 grid((unsigned)cdiv(sh.n1, 64), (unsigned)cdiv(N, 64));
-  const int smem = 2 * 64 * 65 * (int)sizeof(T);
+  constexpr int RA = 8, CB = sizeof(T) == 4 ? 16 : 8;
+  const int64_t nrb = cdiv(sh.n1, 32 * RA);
+  const int64_t kp = cdiv(sh.r0, 16 / (int64_t)sizeof(T)) * (16 / (int64_t)sizeof(T));
+  const size_t smem = ((size_t)kp * 32 * RA + 2 * (size_t)kp * 8 * CB) * sizeof(T);
   static bool attr = false;
   if (!attr) {
-    TR_CUDA(cudaFuncSetAttribute(k_gemm_expand<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 smem));
+    TR_CUDA(cudaFuncSetAttribute(k_gemm_expand<T, RA, CB>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)((64 * 32 * RA + 2 * 64 * 8 * CB) * sizeof(T))));
     attr = true;
   }
-  launch("gemm_expand", k_gemm_expand<T>, grid, 256, smem, st, bf.F0t, sh.n1, (int)sh.r0, bf.C1, N, out);
+  // one resident CTA per SM, a whole number of CTAs per row block
+  const int64_t per_rb = std::max<int64_t>(1, std::min<int64_t>(cdiv(N, 8 * CB), num_sms() / nrb));
+  launch("gemm_expand", k_gemm_expand<T, RA, CB>, (unsigned)(per_rb * nrb), 256, smem, st, bf.F0t,
+         sh.n1, (int)sh.r0, bf.C1, N, out);
   TR_LAUNCH_CHECK();
   return 0;
 }

@@ -378,30 +378,45 @@ __global__ void __launch_bounds__(512) k_ritz(const double* __restrict__ Mfull, 
         cs_s[threadIdx.x] = sn;
       }
       __syncthreads();
-      // columns: A <- A J, Q <- Q J
-      for (int e = threadIdx.x; e < npairs * 64; e += blockDim.x) {
-        const int k = e / 64, i = e % 64;
-        const int p = pp[k], q = pq[k];
-        const double c = cs_c[k], sn = cs_s[k];
-        if (sn != 0.0) {
-          const double ap = A[i + ld * p], aq = A[i + ld * q];
-          A[i + ld * p] = c * ap - sn * aq;
-          A[i + ld * q] = sn * ap + c * aq;
+      // one pass per round: the rotations of a round act on disjoint index
+      // pairs, so J^T A J splits into independent 2x2 blocks
+      // B'(k1,k2) = J_k1^T B(k1,k2) J_k2 (upper blocks, mirrored), and Q <- Q J
+      // row by row; only the live n x n part is touched.
+      for (int e = threadIdx.x; e < npairs * npairs + npairs * n; e += blockDim.x) {
+        if (e < npairs * npairs) {
+          const int k1 = e / npairs, k2 = e - k1 * npairs;
+          if (k1 > k2) continue;
+          const double s1 = cs_s[k1], s2 = cs_s[k2];
+          if (s1 == 0.0 && s2 == 0.0) continue;
+          const double c1 = cs_c[k1], c2 = cs_c[k2];
+          const int p1 = pp[k1], q1 = pq[k1], p2 = pp[k2], q2 = pq[k2];
+          const double a = A[p1 + ld * p2], b = A[p1 + ld * q2];
+          const double c = A[q1 + ld * p2], d = A[q1 + ld * q2];
+          // columns (B J2), then rows (J1^T .)
+          const double ap = c2 * a - s2 * b, bq = s2 * a + c2 * b;
+          const double cp = c2 * c - s2 * d, dq = s2 * c + c2 * d;
+          const double npp = c1 * ap - s1 * cp, npq = c1 * bq - s1 * dq;
+          const double nqp = s1 * ap + c1 * cp, nqq = s1 * bq + c1 * dq;
+          A[p1 + ld * p2] = npp;
+          A[p1 + ld * q2] = npq;
+          A[q1 + ld * p2] = nqp;
+          A[q1 + ld * q2] = nqq;
+          if (k1 != k2) {
+            A[p2 + ld * p1] = npp;
+            A[q2 + ld * p1] = npq;
+            A[p2 + ld * q1] = nqp;
+            A[q2 + ld * q1] = nqq;
+          }
+        } else {
+          const int e2 = e - npairs * npairs;
+          const int k = e2 / n, i = e2 - k * n;
+          const double sn = cs_s[k];
+          if (sn == 0.0) continue;
+          const double c = cs_c[k];
+          const int p = pp[k], q = pq[k];
           const double qp = Q[i + ld * p], qq = Q[i + ld * q];
           Q[i + ld * p] = c * qp - sn * qq;
           Q[i + ld * q] = sn * qp + c * qq;
-        }
-      }
-      __syncthreads();
-      // rows: A <- J^T A
-      for (int e = threadIdx.x; e < npairs * 64; e += blockDim.x) {
-        const int k = e / 64, j = e % 64;
-        const int p = pp[k], q = pq[k];
-        const double c = cs_c[k], sn = cs_s[k];
-        if (sn != 0.0) {
-          const double ap = A[p + ld * j], aq = A[q + ld * j];
-          A[p + ld * j] = c * ap - sn * aq;
-          A[q + ld * j] = sn * ap + c * aq;
         }
       }
       __syncthreads();
@@ -543,49 +558,103 @@ __global__ void k_expand_mode1(const double* __restrict__ core, int r0, int r1, 
 }
 
 // out (n1 x N, col-major) = F0 (n1 x K) * C1 (K x N); K <= 64.
-// 64x64 CTA tile, 256 threads, 4x4 register tile per thread.
-template <typename T>
-__global__ void __launch_bounds__(256) k_gemm_expand(const T* __restrict__ F0, int64_t n1,
-                                                     int K, const T* __restrict__ C1,
-                                                     int64_t N, T* __restrict__ out) {
+// Persistent CTAs, each pinned to one block of 32*RA rows whose F0 rows stay
+// in shared memory, looping over (8*CB)-column tiles of C1 (double-buffered
+// with cp.async).  Thread (lane, warp) owns rows lane + 32a (a < RA: coalesced
+// stores) and columns CB*warp + b (b < CB: broadcast shared reads).  Both
+// operands are stored k-contiguous with K padded to Kp (a multiple of the
+// 16-byte vector width VK), so VK consecutive k come in one 16-byte load:
+// per VK k-steps a thread issues RA + CB vector loads for VK*RA*CB FMAs.
+template <typename T, int RA, int CB>
+__global__ void __launch_bounds__(256, 1) k_gemm_expand(const T* __restrict__ F0, int64_t n1,
+                                                        int K, const T* __restrict__ C1,
+                                                        int64_t N, T* __restrict__ out) {
+  constexpr int ROWS = 32 * RA, COLS = 8 * CB, VK = 16 / (int)sizeof(T);
+  using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
   extern __shared__ __align__(16) unsigned char gemm_smem[];
-  T(*fa)[65] = reinterpret_cast<T(*)[65]>(gemm_smem);                    // [k][row]
-  T(*cb)[65] = reinterpret_cast<T(*)[65]>(gemm_smem + 64 * 65 * sizeof(T));  // [k][col]
-  const int64_t r0 = (int64_t)blockIdx.x * 64, c0 = (int64_t)blockIdx.y * 64;
-  for (int e = threadIdx.x; e < 64 * 64; e += 256) {
-    const int i = e % 64, k = e / 64;
-    fa[k][i] = (k < K && r0 + i < n1) ? F0[r0 + i + n1 * k] : T(0);
-    const int kk = e % 64, j = e / 64;
-    cb[kk][j] = (kk < K && c0 + j < N) ? C1[kk + (int64_t)K * (c0 + j)] : T(0);
-  }
+  const int Kp = (K + VK - 1) / VK * VK;
+  T* fa = reinterpret_cast<T*>(gemm_smem);  // [row][Kp]
+  T* cbuf = fa + (size_t)ROWS * Kp;         // 2 x [col][Kp]
+  const int tile_el = COLS * Kp;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nrb = (n1 + ROWS - 1) / ROWS, nct = (N + COLS - 1) / COLS;
+  const int64_t rb = blockIdx.x % nrb, cstep = gridDim.x / nrb;
+  const int64_t r0 = rb * ROWS;
+  if ((int64_t)blockIdx.x >= cstep * nrb) return;
+  for (int e = threadIdx.x; e < 2 * tile_el; e += blockDim.x) cbuf[e] = T(0);  // k padding
   __syncthreads();
-  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  T acc[4][4];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = T(0);
-  for (int k = 0; k < K; ++k) {
-    T fr[4], cr[4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a) fr[a] = fa[k][tx + 16 * a];
-#pragma unroll
-    for (int b = 0; b < 4; ++b) cr[b] = cb[k][ty + 16 * b];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b] += fr[a] * cr[b];
-  }
-#pragma unroll
-  for (int b = 0; b < 4; ++b) {
-    const int64_t col = c0 + ty + 16 * b;
-    if (col >= N) continue;
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int64_t row = r0 + tx + 16 * a;
-      if (row < n1) out[row + n1 * col] = acc[a][b];
+  // C1 tile ct -> buffer (column j, k) at j*Kp + k; columns past N zeroed
+  auto fill = [&](int64_t ct, T* dst) {
+    if (ct < nct) {
+      const int64_t c0 = ct * COLS;
+      const int ncol = (int)((N - c0) < COLS ? (N - c0) : COLS);
+      const T* src = C1 + (int64_t)K * c0;
+      const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+      for (int e = threadIdx.x; e < ncol * K; e += blockDim.x) {
+        const int j = e / K, k = e - j * K;
+        if (sizeof(T) == 4) cpa4(d + (j * Kp + k) * 4, src + e);
+        else cpa8(d + (j * Kp + k) * 8, src + e);
+      }
+      for (int e = ncol * Kp + threadIdx.x; e < tile_el; e += blockDim.x) dst[e] = T(0);
     }
+    cpa_commit();
+  };
+  int64_t ct = blockIdx.x / nrb;
+  fill(ct, cbuf);
+  for (int e = threadIdx.x; e < ROWS * Kp; e += blockDim.x) {
+    const int i = e / Kp, k = e - i * Kp;
+    fa[e] = (r0 + i < n1 && k < K) ? F0[r0 + i + n1 * k] : T(0);
   }
+  for (int buf = 0; ct < nct; ct += cstep, buf ^= 1) {
+    fill(ct + cstep, cbuf + (buf ^ 1) * tile_el);
+    cpa_wait1();
+    __syncthreads();
+    const T* cb = cbuf + buf * tile_el + (size_t)Kp * CB * warp;  // this warp's columns
+    T acc[RA][CB];
+#pragma unroll
+    for (int a = 0; a < RA; ++a)
+#pragma unroll
+      for (int b = 0; b < CB; ++b) acc[a][b] = T(0);
+    for (int k0 = 0; k0 < Kp; k0 += VK) {
+      T fr[RA][VK];
+#pragma unroll
+      for (int a = 0; a < RA; ++a) {
+        const V v = *reinterpret_cast<const V*>(fa + (lane + 32 * a) * Kp + k0);
+        if constexpr (VK == 4) {
+          fr[a][0] = v.x; fr[a][1] = v.y; fr[a][2] = v.z; fr[a][3] = v.w;
+        } else {
+          fr[a][0] = v.x; fr[a][1] = v.y;
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < CB; ++b) {
+        const V w = *reinterpret_cast<const V*>(cb + b * Kp + k0);
+        T cr[VK];
+        if constexpr (VK == 4) {
+          cr[0] = w.x; cr[1] = w.y; cr[2] = w.z; cr[3] = w.w;
+        } else {
+          cr[0] = w.x; cr[1] = w.y;
+        }
+#pragma unroll
+        for (int kk = 0; kk < VK; ++kk)
+#pragma unroll
+          for (int a = 0; a < RA; ++a) acc[a][b] += fr[a][kk] * cr[kk];
+      }
+    }
+    const int64_t c0 = ct * COLS;
+#pragma unroll
+    for (int b = 0; b < CB; ++b) {
+      const int64_t col = c0 + CB * warp + b;
+      if (col >= N) continue;
+#pragma unroll
+      for (int a = 0; a < RA; ++a) {
+        const int64_t row = r0 + lane + 32 * a;
+        if (row < n1) out[row + n1 * col] = acc[a][b];
+      }
+    }
+    __syncthreads();  // buffer `buf` is refilled next iteration
+  }
+  cpa_wait0();
 }
 
 }  // namespace tr
