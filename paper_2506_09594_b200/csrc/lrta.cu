@@ -279,21 +279,63 @@ static void orth_basis(int64_t m, int s, Bufs<T>& bf, int64_t* info, cudaStream_
 
 // W = A^T Z and M = W^T W on the tensor cores (proj_tc.cuh) for fp32
 // unfoldings with m % 32 == 0 and s <= 32; returns false to use the generic path.
+// cuTensorMapEncodeTiled from the driver (no libcuda link dependency)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+    cudaGetLastError();
+  }
+  return fn;
+}
+
+// fp32 column-major rows x cols matrix, boxes of 32 rows x box_cols columns,
+// 128-byte swizzle (one box row = 32 fp32 = one swizzle atom), zero OOB fill
+static bool tmap_f32(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int box_cols) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)cols};
+  const cuuint64_t strides[1] = {(cuuint64_t)rows * sizeof(float)};
+  const cuuint32_t box[2] = {32, (cuuint32_t)box_cols};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// W = A^T Z on the tensor cores (proj_tc.cuh) when the unfolding suits it
 static bool project(const float* A, int64_t m, int64_t n, int s, Bufs<float>& bf, cudaStream_t st) {
-  if (m % 32 != 0 || s > 32 || ((uintptr_t)A % 16) != 0 || getenv("TR_NO_TC") != nullptr)
+  if (m % 32 != 0 || s > 32 || ((uintptr_t)A % 16) != 0 || n >= (1ll << 31) ||
+      getenv("TR_NO_TC") != nullptr)
+    return false;
+  CUtensorMap ma, mh, ml;
+  if (!tmap_f32(&ma, A, m, n, 128) || !tmap_f32(&mh, bf.zhi, m, 32, 32) ||
+      !tmap_f32(&ml, bf.zlo, m, 32, 32))
     return false;
   launch("proj_split", k_split_z, (unsigned)cdiv(m * 32, 256), 256, 0, st, bf.Z, m, s, bf.zhi,
          bf.zlo);
   const int64_t ntiles = cdiv(n, 128);
   const int64_t grid = std::min<int64_t>(ntiles, num_sms());
-  const size_t smem = (size_t)kPjStages * kPjStageBytes + 1024;
+  const size_t smem = (size_t)kPwStages * kPwStageBytes + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_proj_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_proj_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  launch("proj_tc", k_proj_tc, (unsigned)grid, kPjThreads, smem, st, A, m, n, bf.zhi, bf.zlo, s,
-         bf.W, bf.Mpart);
+  launch("proj_tc", k_proj_ws, (unsigned)grid, kPwThreads, smem, st, ma, mh, ml, m, n, s, bf.W,
+         bf.Mpart);
   reduce(bf.Mpart, grid, (int64_t)s * s, bf.M, st);
   return true;
 }
@@ -332,8 +374,11 @@ static int bki_mode(const T* A, int64_t m, int64_t n, int r, int b, int q, Sketc
     const int64_t mparts = std::min<int64_t>(cdiv(n, 64), bf.max_mparts);
     const int64_t rpb = cdiv(n, mparts);
     const int64_t mp = cdiv(n, rpb);
-    launch("wtw", k_wtw<T>, (unsigned)mp, 256, 32 * s * sizeof(double), st, bf.W, n, s, rpb,
-           bf.Mpart);
+    if (s <= 32)
+      launch("wtw", k_wtw32<T>, (unsigned)mp, 256, 0, st, (const T*)bf.W, n, s, rpb, bf.Mpart);
+    else
+      launch("wtw", k_wtw<T>, (unsigned)mp, 256, 32 * s * sizeof(double), st, bf.W, n, s, rpb,
+             bf.Mpart);
     reduce(bf.Mpart, mp, (int64_t)s * s, bf.M, st);
   }
   if (s <= kJW && g_use_warp_jacobi) {

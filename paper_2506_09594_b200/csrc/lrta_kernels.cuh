@@ -140,6 +140,57 @@ __global__ void __launch_bounds__(256) k_wtw(const T* __restrict__ W, int64_t n,
   }
 }
 
+// Same partials for s <= 32: thread t of each 64-thread row group owns the
+// 4 x 4 block (4 (t/8) + a, 4 (t%8) + b) of the Gram, 16 independent fp64
+// accumulators; the 4 row groups of the CTA are combined in shared memory.
+template <typename T>
+__global__ void __launch_bounds__(256) k_wtw32(const T* __restrict__ W, int64_t n, int s,
+                                               int64_t rows_per_blk, double* __restrict__ part) {
+  __shared__ double red[3][32 * 32];
+  const int grp = threadIdx.x >> 6, t = threadIdx.x & 63;
+  const int j0 = 4 * (t >> 3), k0 = 4 * (t & 7);
+  const int64_t rb = (int64_t)blockIdx.x * rows_per_blk;
+  const int64_t re = min(n, rb + rows_per_blk);
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  if (j0 < s && k0 < s) {
+    for (int64_t r = rb + grp; r < re; r += 4) {
+      const T* row = W + r * s;
+      double x[4], y[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        x[a] = j0 + a < s ? (double)row[j0 + a] : 0.0;
+        y[a] = k0 + a < s ? (double)row[k0 + a] : 0.0;
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] += x[a] * y[b];
+    }
+  }
+  if (grp > 0)
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) red[grp - 1][(j0 + a) * 32 + k0 + b] = acc[a][b];
+  __syncthreads();
+  if (grp == 0)
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int j = j0 + a, k = k0 + b;
+        if (j < s && k < s) {
+          const int e = j * 32 + k;
+          part[(int64_t)blockIdx.x * s * s + j * s + k] =
+              ((acc[a][b] + red[0][e]) + red[1][e]) + red[2][e];
+        }
+      }
+}
+
 // out[e] = sum_p part[p*len + e]  (fixed summation order: deterministic).
 // One warp per 32 consecutive outputs x 8 partial groups: lanes stream
 // coalesced rows, each warp owns a slice of the partials, smem tree at the end.

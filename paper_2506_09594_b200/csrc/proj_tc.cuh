@@ -2,45 +2,31 @@
 //
 // tenrec/sketch.py:262-263 forms w = a^T z (n x s) and m = w^T w for the
 // Rayleigh-Ritz step; s = (q+1) b is 20-40, so this is the one genuinely dense
-// contraction of the Krylov iteration (2s flops per streamed element).  Here:
-//   * A tile  = 128 columns of the unfolding x 32 rows (K), K-major, 128B
-//     swizzle, filled by cp.async; its low part A_lo = A - tf32(A) is written
-//     next to it by the threads (3xTF32: A Z_hi + A Z_lo + A_lo Z_hi, fp32-
-//     faithful; the tensor core truncates fp32 operands to tf32).
-//   * Z_hi / Z_lo tiles = 32 (N, s padded) x 32 rows, same layout.
-//   * tcgen05.mma.cta_group::1.kind::tf32, M=128 N=32 K=8, accumulator in TMEM
-//     (32 columns), issued by one thread; tcgen05.commit releases each stage.
-//   * epilogue per 128-column tile: tcgen05.ld -> W rows to HBM, and the
-//     32 x 32 Gram W^T W of the tile accumulated in fp64 (the per-CTA partial
-//     of M), so no separate pass over W is needed.
+// contraction of the Krylov iteration (2s flops per streamed element).
+// Warp-specialised persistent kernel, one CTA per SM:
+//   warp 0     TMA producer: A tile = 128 columns of the unfolding x 32 rows
+//              (K), K-major 128B-swizzled by the tensor map, plus the matching
+//              32-row chunks of Z_hi / Z_lo, into a kPwStages-deep ring;
+//   warps 2-5  split A_lo = A - tf32(A) next to each landed tile (3xTF32:
+//              A Z_hi + A Z_lo + A_lo Z_hi, fp32-faithful);
+//   warp 1     one thread issues tcgen05.mma.cta_group::1.kind::tf32
+//              (M=128 N=32 K=8) into a double-buffered TMEM accumulator and
+//              frees ring slots with tcgen05.commit;
+//   warps 6-9  epilogue: tcgen05.ld of a finished tile -> W rows in HBM and
+//              the tile's 32 x 32 Gram W^T W accumulated in fp64 (the per-CTA
+//              partial of M), while the next tile accumulates in the other
+//              TMEM buffer.
 #pragma once
+
+#include <cuda.h>
 
 #include "common.cuh"
 #include "panel.cuh"
 
 namespace tr {
 
-constexpr int kPjThreads = 128;
-constexpr int kPjStages = 4;
 constexpr int kPjTileBytes = 128 * 128;  // A tile: 128 rows x 128 B
 constexpr int kPjZBytes = 32 * 128;      // Z tile: 32 rows x 128 B
-constexpr int kPjStageBytes = 2 * kPjTileBytes + 2 * kPjZBytes;
-
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
-  const int sz = valid ? 16 : 0;  // zero-fill when out of range
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(sz)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-// byte offset of 16-byte chunk q of row r in a K-major SWIZZLE_128B tile
-__device__ __forceinline__ uint32_t sw128(int r, int q) {
-  return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((q ^ (r & 7)) << 4));
-}
 
 // UMMA shared-memory descriptor: K-major, SWIZZLE_128B, SBO = 1024 B (8-row atoms)
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
@@ -109,157 +95,175 @@ __global__ void k_split_z(const double* __restrict__ Z, int64_t m, int s,
   zlo[e] = (float)(z - (double)hi);
 }
 
-// W (n x s row-major) = A^T Z ; part[blk] (32 x 32, fp64) = sum over this CTA's
-// columns of w w^T.  Requires m % 32 == 0 and 16-byte aligned A.
-__global__ void __launch_bounds__(kPjThreads, 1)
-    k_proj_tc(const float* __restrict__ A, int64_t m, int64_t n, const float* __restrict__ zhi,
-              const float* __restrict__ zlo, int s, float* __restrict__ W,
-              double* __restrict__ part) {
-  extern __shared__ __align__(1024) unsigned char pj_raw[];
-  __shared__ __align__(8) uint64_t mma_done[kPjStages];
-  __shared__ __align__(8) uint64_t acc_ready;
+constexpr int kPwStages = 5;
+constexpr int kPwThreads = 320;
+constexpr int kPwStageBytes = 2 * kPjTileBytes + 2 * kPjZBytes;  // A, A_lo, Z_hi, Z_lo
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(dst),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// W (n x s row-major) = A^T Z and part[blk] = this CTA's share of W^T W (s x s,
+// fp64).  A: m x n column-major (tensor map mapA, box 32 x 128); Z_hi / Z_lo:
+// m x 32 column-major (maps, box 32 x 32).  m % 32 == 0.
+__global__ void __launch_bounds__(kPwThreads, 1)
+    k_proj_ws(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapZh,
+              const __grid_constant__ CUtensorMap mapZl, int64_t m, int64_t n, int s,
+              float* __restrict__ W, double* __restrict__ part) {
+  extern __shared__ __align__(1024) unsigned char pw_raw[];
+  __shared__ __align__(8) uint64_t full[kPwStages], lo_ready[kPwStages], empty[kPwStages];
+  __shared__ __align__(8) uint64_t tfull[2], tempty[2];
   __shared__ uint32_t tmem_base_s;
-  __shared__ float wtile[128][33];
-  unsigned char* smem = (unsigned char*)(((uintptr_t)pj_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* smem = (unsigned char*)(((uintptr_t)pw_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = smem_u32(smem);
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntiles = (n + 127) / 128;
   const int kt = (int)(m / 32);
   const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t iters = my_tiles * kt;
 
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(
         smem_u32(&tmem_base_s)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (tid == 0) {
-    for (int i = 0; i < kPjStages; ++i) mbar_init(&mma_done[i], 1);
-    mbar_init(&acc_ready, 1);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kPwStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&lo_ready[i], 128);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 128);
+    }
     fence_barrier_init();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_s;
-  const uint32_t idesc = idesc_tf32(128, 32);
 
-  // issue the cp.async loads of iteration `it` into its stage
-  auto load = [&](int64_t it) {
-    if (it < iters) {
-      const int64_t tile = blockIdx.x + (it / kt) * gridDim.x;
-      const int64_t k0 = (it % kt) * 32;
-      const int64_t c0 = tile * 128;
-      const uint32_t st = sbase + (uint32_t)((it % kPjStages) * kPjStageBytes);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {  // A: 128 rows x 8 chunks
-        const int e = tid + kPjThreads * u;
-        const int r = e >> 3, q = e & 7;
-        const int64_t col = c0 + r;
-        const bool ok = col < n;
-        cp_async16(st + sw128(r, q), A + (ok ? col : 0) * m + k0 + 4 * q, ok);
-      }
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {  // Z_hi, Z_lo: 32 rows x 8 chunks each
-        const int e = tid + kPjThreads * u;
-        const int r = e >> 3, q = e & 7;
-        cp_async16(st + 2 * kPjTileBytes + sw128(r, q), zhi + (int64_t)r * m + k0 + 4 * q, true);
-        cp_async16(st + 2 * kPjTileBytes + kPjZBytes + sw128(r, q), zlo + (int64_t)r * m + k0 + 4 * q,
-                   true);
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer ----
+      for (int64_t it = 0; it < iters; ++it) {
+        const int st = (int)(it % kPwStages);
+        const uint32_t ph = (uint32_t)((it / kPwStages) & 1);
+        mbar_wait(&empty[st], ph ^ 1);
+        const int64_t tile = blockIdx.x + (it / kt) * gridDim.x;
+        const int k0 = (int)((it % kt) * 32);
+        const uint32_t sa = sbase + (uint32_t)(st * kPwStageBytes);
+        mbar_arrive_expect_tx(&full[st], kPjTileBytes + 2 * kPjZBytes);
+        tma_load_2d(sa, &mapA, k0, (int)(tile * 128), &full[st]);
+        tma_load_2d(sa + 2 * kPjTileBytes, &mapZh, k0, 0, &full[st]);
+        tma_load_2d(sa + 2 * kPjTileBytes + kPjZBytes, &mapZl, k0, 0, &full[st]);
       }
     }
-    cp_async_commit();
-  };
-
-  for (int i = 0; i < kPjStages - 1; ++i) load(i);
-  double g[8];
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer ----
+      const uint32_t idesc = idesc_tf32(128, 32);
+      for (int64_t t = 0; t < my_tiles; ++t) {
+        const int acc = (int)(t & 1);
+        mbar_wait(&tempty[acc], (uint32_t)(((t >> 1) & 1) ^ 1));
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(acc * 32);
+        for (int kk = 0; kk < kt; ++kk) {
+          const int64_t it = t * kt + kk;
+          const int st = (int)(it % kPwStages);
+          mbar_wait(&lo_ready[st], (uint32_t)((it / kPwStages) & 1));
+          tc_fence_after();
+          const uint32_t sa = sbase + (uint32_t)(st * kPwStageBytes);
+          const uint64_t dA = umma_desc_sw128(sa);
+          const uint64_t dAl = umma_desc_sw128(sa + kPjTileBytes);
+          const uint64_t dZh = umma_desc_sw128(sa + 2 * kPjTileBytes);
+          const uint64_t dZl = umma_desc_sw128(sa + 2 * kPjTileBytes + kPjZBytes);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) g[i] = 0.0;
-  uint32_t acc_phase = 0;
-
-  for (int64_t it = 0; it < iters; ++it) {
-    const int sidx = (int)(it % kPjStages);
-    const uint32_t st = sbase + (uint32_t)(sidx * kPjStageBytes);
-    // refill the stage consumed by the previous iteration (its MMAs are older)
-    if (it >= 1) {
-      const int64_t prev = it - 1;
-      mbar_wait(&mma_done[prev % kPjStages], (uint32_t)((prev / kPjStages) & 1));
-    }
-    load(it + kPjStages - 1);
-    cp_async_wait<kPjStages - 1>();
-    // A_lo = A - tf32(A) for this thread's chunks
-    unsigned char* sp = smem + sidx * kPjStageBytes;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int e = tid + kPjThreads * u;
-      const uint32_t off = sw128(e >> 3, e & 7);
-      const float4 a = *reinterpret_cast<const float4*>(sp + off);
-      float4 lo;
-      lo.x = a.x - __uint_as_float(__float_as_uint(a.x) & 0xFFFFE000u);
-      lo.y = a.y - __uint_as_float(__float_as_uint(a.y) & 0xFFFFE000u);
-      lo.z = a.z - __uint_as_float(__float_as_uint(a.z) & 0xFFFFE000u);
-      lo.w = a.w - __uint_as_float(__float_as_uint(a.w) & 0xFFFFE000u);
-      *reinterpret_cast<float4*>(sp + kPjTileBytes + off) = lo;
-    }
-    fence_async_smem();
-    __syncthreads();
-    const bool first_k = (it % kt) == 0;
-    const bool last_k = (it % kt) == kt - 1;
-    if (tid == 0) {
-      tc_fence_after();
-      const uint64_t dA = umma_desc_sw128(st);
-      const uint64_t dAl = umma_desc_sw128(st + kPjTileBytes);
-      const uint64_t dZh = umma_desc_sw128(st + 2 * kPjTileBytes);
-      const uint64_t dZl = umma_desc_sw128(st + 2 * kPjTileBytes + kPjZBytes);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {  // K = 8 per MMA: +32 B in the swizzled row
-        const uint64_t adv = (uint64_t)(2 * k);
-        umma_tf32(tmem, dA + adv, dZh + adv, idesc, (first_k && k == 0) ? 0u : 1u);
-        umma_tf32(tmem, dA + adv, dZl + adv, idesc, 1u);
-        umma_tf32(tmem, dAl + adv, dZh + adv, idesc, 1u);
+          for (int k = 0; k < 4; ++k) {  // K = 8 per MMA: +32 B in the swizzled row
+            const uint64_t adv = (uint64_t)(2 * k);
+            umma_tf32(d, dA + adv, dZh + adv, idesc, (kk == 0 && k == 0) ? 0u : 1u);
+            umma_tf32(d, dA + adv, dZl + adv, idesc, 1u);
+            umma_tf32(d, dAl + adv, dZh + adv, idesc, 1u);
+          }
+          umma_commit(&empty[st]);
+        }
+        umma_commit(&tfull[acc]);
       }
-      umma_commit(&mma_done[sidx]);
-      if (last_k) umma_commit(&acc_ready);
     }
-    if (last_k) {
-      mbar_wait(&acc_ready, acc_phase);
-      acc_phase ^= 1;
-      tc_fence_after();
-      float w[32];
-      tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16), w);
-      const int64_t tile = blockIdx.x + (it / kt) * gridDim.x;
-      const int64_t col = tile * 128 + tid;
-      if (col < n) {
-        for (int j = 0; j < s; ++j) W[col * s + j] = w[j];
-      }
-#pragma unroll
-      for (int j = 0; j < 32; ++j) wtile[tid][j] = (col < n) ? w[j] : 0.f;
-      tc_fence_before();
-      __syncthreads();
-      // tile Gram: thread owns 8 entries e = tid + 128 u of the 32 x 32 block
+  } else if (warp < 6) {  // ---- A_lo split ----
+    const int ct = threadIdx.x - 64;
+    for (int64_t it = 0; it < iters; ++it) {
+      const int st = (int)(it % kPwStages);
+      mbar_wait(&full[st], (uint32_t)((it / kPwStages) & 1));
+      unsigned char* sp = smem + st * kPwStageBytes;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int e = tid + kPjThreads * u;
-        const int j = e >> 5, k = e & 31;
-        double a = 0.0;
-        for (int r = 0; r < 128; ++r) a += (double)wtile[r][j] * (double)wtile[r][k];
-        g[u] += a;
+        const uint32_t off = (uint32_t)(ct + 128 * u) * 16u;  // swizzle-agnostic: same offset
+        const float4 a = *reinterpret_cast<const float4*>(sp + off);
+        float4 lo;
+        lo.x = a.x - __uint_as_float(__float_as_uint(a.x) & 0xFFFFE000u);
+        lo.y = a.y - __uint_as_float(__float_as_uint(a.y) & 0xFFFFE000u);
+        lo.z = a.z - __uint_as_float(__float_as_uint(a.z) & 0xFFFFE000u);
+        lo.w = a.w - __uint_as_float(__float_as_uint(a.w) & 0xFFFFE000u);
+        *reinterpret_cast<float4*>(sp + kPjTileBytes + off) = lo;
       }
-      __syncthreads();
+      fence_async_smem();
+      mbar_arrive(&lo_ready[st]);
     }
-  }
-  cp_async_wait<0>();
+  } else {  // ---- epilogue: TMEM lane quarter (warp % 4) ----
+    __shared__ float wt[128][33];
+    const int q = warp & 3;
+    const int row = 32 * q + lane;
+    const int et = threadIdx.x - 192;  // 0..127: Gram entries et + 128 u
+    double g[8];
 #pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    const int e = tid + kPjThreads * u;
-    const int j = e >> 5, k = e & 31;
-    if (j < s && k < s) part[(int64_t)blockIdx.x * s * s + j * s + k] = g[u];
+    for (int u = 0; u < 8; ++u) g[u] = 0.0;
+    for (int64_t t = 0; t < my_tiles; ++t) {
+      const int acc = (int)(t & 1);
+      mbar_wait(&tfull[acc], (uint32_t)((t >> 1) & 1));
+      tc_fence_after();
+      float w[32];
+      tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * 32), w);
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      const int64_t col = (blockIdx.x + t * gridDim.x) * 128 + row;
+      if (col < n) {
+        float* dst = W + col * s;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < s) dst[j] = w[j];
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile's Gram reads done
+#pragma unroll
+      for (int j = 0; j < 32; ++j) wt[row][j] = col < n ? w[j] : 0.f;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      for (int r = 0; r < 128; ++r) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = et + 128 * u;
+          g[u] += (double)wt[r][e >> 5] * (double)wt[r][e & 31];
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = et + 128 * u, j = e >> 5, k = e & 31;
+      if (j < s && k < s) part[(int64_t)blockIdx.x * s * s + j * s + k] = g[u];
+    }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) {
+  if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
   }
 }
 
