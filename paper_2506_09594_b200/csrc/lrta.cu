@@ -328,7 +328,7 @@ static bool project(const float* A, int64_t m, int64_t n, int s, Bufs<float>& bf
          bf.zlo);
   const int64_t ntiles = cdiv(n, 128);
   const int64_t grid = std::min<int64_t>(ntiles, num_sms());
-  const size_t smem = (size_t)kPwStages * kPwStageBytes + 1024;
+  const size_t smem = (size_t)kPwSmemBytes + 1024;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_proj_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -95,9 +95,11 @@ __global__ void k_split_z(const double* __restrict__ Z, int64_t m, int s,
   zlo[e] = (float)(z - (double)hi);
 }
 
-constexpr int kPwStages = 5;
+constexpr int kPwStages = 6;   // TMA ring: A, Z_hi, Z_lo
+constexpr int kPwLo = 4;       // A_lo ring (split warps -> MMA)
 constexpr int kPwThreads = 320;
-constexpr int kPwStageBytes = 2 * kPjTileBytes + 2 * kPjZBytes;  // A, A_lo, Z_hi, Z_lo
+constexpr int kPwStageBytes = kPjTileBytes + 2 * kPjZBytes;
+constexpr int kPwSmemBytes = kPwStages * kPwStageBytes + kPwLo * kPjTileBytes;
 
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
                                             uint64_t* bar) {
@@ -120,7 +122,8 @@ __global__ void __launch_bounds__(kPwThreads, 1)
               const __grid_constant__ CUtensorMap mapZl, int64_t m, int64_t n, int s,
               float* __restrict__ W, double* __restrict__ part) {
   extern __shared__ __align__(1024) unsigned char pw_raw[];
-  __shared__ __align__(8) uint64_t full[kPwStages], lo_ready[kPwStages], empty[kPwStages];
+  __shared__ __align__(8) uint64_t full[kPwStages], empty[kPwStages];
+  __shared__ __align__(8) uint64_t lo_ready[kPwLo], lo_empty[kPwLo];
   __shared__ __align__(8) uint64_t tfull[2], tempty[2];
   __shared__ uint32_t tmem_base_s;
   unsigned char* smem = (unsigned char*)(((uintptr_t)pw_raw + 1023) & ~(uintptr_t)1023);
@@ -139,8 +142,11 @@ __global__ void __launch_bounds__(kPwThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < kPwStages; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&lo_ready[i], 128);
       mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < kPwLo; ++i) {
+      mbar_init(&lo_ready[i], 128);
+      mbar_init(&lo_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
@@ -164,8 +170,8 @@ __global__ void __launch_bounds__(kPwThreads, 1)
         const uint32_t sa = sbase + (uint32_t)(st * kPwStageBytes);
         mbar_arrive_expect_tx(&full[st], kPjTileBytes + 2 * kPjZBytes);
         tma_load_2d(sa, &mapA, k0, (int)(tile * 128), &full[st]);
-        tma_load_2d(sa + 2 * kPjTileBytes, &mapZh, k0, 0, &full[st]);
-        tma_load_2d(sa + 2 * kPjTileBytes + kPjZBytes, &mapZl, k0, 0, &full[st]);
+        tma_load_2d(sa + kPjTileBytes, &mapZh, k0, 0, &full[st]);
+        tma_load_2d(sa + kPjTileBytes + kPjZBytes, &mapZl, k0, 0, &full[st]);
       }
     }
   } else if (warp == 1) {
@@ -179,13 +185,15 @@ __global__ void __launch_bounds__(kPwThreads, 1)
         for (int kk = 0; kk < kt; ++kk) {
           const int64_t it = t * kt + kk;
           const int st = (int)(it % kPwStages);
-          mbar_wait(&lo_ready[st], (uint32_t)((it / kPwStages) & 1));
+          const int ls = (int)(it % kPwLo);
+          mbar_wait(&lo_ready[ls], (uint32_t)((it / kPwLo) & 1));
           tc_fence_after();
           const uint32_t sa = sbase + (uint32_t)(st * kPwStageBytes);
           const uint64_t dA = umma_desc_sw128(sa);
-          const uint64_t dAl = umma_desc_sw128(sa + kPjTileBytes);
-          const uint64_t dZh = umma_desc_sw128(sa + 2 * kPjTileBytes);
-          const uint64_t dZl = umma_desc_sw128(sa + 2 * kPjTileBytes + kPjZBytes);
+          const uint64_t dAl =
+              umma_desc_sw128(sbase + (uint32_t)(kPwStages * kPwStageBytes + ls * kPjTileBytes));
+          const uint64_t dZh = umma_desc_sw128(sa + kPjTileBytes);
+          const uint64_t dZl = umma_desc_sw128(sa + kPjTileBytes + kPjZBytes);
 #pragma unroll
           for (int k = 0; k < 4; ++k) {  // K = 8 per MMA: +32 B in the swizzled row
             const uint64_t adv = (uint64_t)(2 * k);
@@ -194,6 +202,7 @@ __global__ void __launch_bounds__(kPwThreads, 1)
             umma_tf32(d, dAl + adv, dZh + adv, idesc, 1u);
           }
           umma_commit(&empty[st]);
+          umma_commit(&lo_empty[ls]);
         }
         umma_commit(&tfull[acc]);
       }
@@ -202,8 +211,11 @@ __global__ void __launch_bounds__(kPwThreads, 1)
     const int ct = threadIdx.x - 64;
     for (int64_t it = 0; it < iters; ++it) {
       const int st = (int)(it % kPwStages);
+      const int ls = (int)(it % kPwLo);
+      mbar_wait(&lo_empty[ls], (uint32_t)(((it / kPwLo) & 1) ^ 1));
       mbar_wait(&full[st], (uint32_t)((it / kPwStages) & 1));
-      unsigned char* sp = smem + st * kPwStageBytes;
+      const unsigned char* sp = smem + st * kPwStageBytes;
+      unsigned char* lp = smem + kPwStages * kPwStageBytes + ls * kPjTileBytes;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const uint32_t off = (uint32_t)(ct + 128 * u) * 16u;  // swizzle-agnostic: same offset
@@ -213,10 +225,10 @@ __global__ void __launch_bounds__(kPwThreads, 1)
         lo.y = a.y - __uint_as_float(__float_as_uint(a.y) & 0xFFFFE000u);
         lo.z = a.z - __uint_as_float(__float_as_uint(a.z) & 0xFFFFE000u);
         lo.w = a.w - __uint_as_float(__float_as_uint(a.w) & 0xFFFFE000u);
-        *reinterpret_cast<float4*>(sp + kPjTileBytes + off) = lo;
+        *reinterpret_cast<float4*>(lp + off) = lo;
       }
       fence_async_smem();
-      mbar_arrive(&lo_ready[st]);
+      mbar_arrive(&lo_ready[ls]);
     }
   } else {  // ---- epilogue: TMEM lane quarter (warp % 4) ----
     __shared__ float wt[128][33];
