@@ -159,7 +159,7 @@ static void fft_pass_p2(int mode, const void* in, void* dst, double scale, int64
   static bool generic_only = getenv("TR_FFT_GENERIC") != nullptr;
   static int occ[13] = {0};  // resident CTAs per SM, per specialised ln (index 12: k_fft_p2)
   FftTileKernel<T> tk = (L * nt == 2048 && !generic_only) ? fft_tile_kernel<T>(ln) : nullptr;
-  const size_t smem = tk ? ((size_t)nt + 2 * (size_t)kFftTileSlots) * sizeof(cpx<T>)
+  const size_t smem = tk ? ((size_t)nt + kFftRtwSlots(nt) + 2 * (size_t)kFftTileSlots) * sizeof(cpx<T>)
                          : ((size_t)nt + 2 * (size_t)L * (nt + 1)) * sizeof(cpx<T>);
   const int slot = tk ? ln : 12;
   if (occ[slot] == 0) {

@@ -786,6 +786,8 @@ struct R8Plan {
 __device__ __forceinline__ int fpad(int i) { return i + (i >> 4); }
 // padded tile slots for a 2048-point tile (+ the C2R staging overhang)
 constexpr int kFftTileSlots = 2048 + 2048 / 16 + 32;
+// slots of the real-transform twiddle table (NT/2 + 1, rounded to 16 bytes x 2)
+__host__ __device__ constexpr int kFftRtwSlots(int nt) { return (nt / 2 + 1 + 1) & ~1; }
 
 // per-stage twiddles of the radix-8/4 plan: stage s holds w^{jm r nt/(Ns R)}
 // at toff(s) + jm (R-1) + r-1
@@ -855,10 +857,13 @@ __device__ __forceinline__ void stockham8(cpx<T>* buf, const cpx<T>* st_tab, boo
       const int l = lo_major ? (e & ((1 << LL) - 1)) : (e >> lg);
       const int b = lo_major ? (e >> LL) : (e & ((1 << lg) - 1));
       const int jm = b & nsm;
+      // read offsets r * 2^lg (x 2^LL when lo-major) are multiples of 16: the
+      // padded slot of element r is p0 + r * (step + step / 16)
+      const int p0 = fpad(lo_major ? (b << LL) + l : (l << LN) + b);
+      const int rstep = lo_major ? (1 << (lg + LL)) : (1 << lg);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const int k = b + (r << lg);
-        cpx<T> x = buf[fpad(lo_major ? (k << LL) + l : (l << LN) + k)];
+        cpx<T> x = buf[p0 + r * (rstep + (rstep >> 4))];
         if (r > 0 && s > 0) {
           cpx<T> w = st_tab[P::toff(s) + jm * (R - 1) + r - 1];
           if (INV) w.im = -w.im;
@@ -876,10 +881,15 @@ __device__ __forceinline__ void stockham8(cpx<T>* buf, const cpx<T>* st_tab, boo
       const int l = lo_major ? (e & ((1 << LL) - 1)) : (e >> lg);
       const int b = lo_major ? (e >> LL) : (e & ((1 << lg) - 1));
       const int base = ((b >> lNs) << (lNs + lR)) + (b & nsm);
+      const int i0 = lo_major ? (base << LL) + l : (l << LN) + base;
+      const int wstep = lo_major ? (1 << (lNs + LL)) : (1 << lNs);
+      if ((wstep & 15) == 0) {
+        const int q0 = fpad(i0);
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int k = base + (r << lNs);
-        buf[fpad(lo_major ? (k << LL) + l : (l << LN) + k)] = v[g * R + r];
+        for (int r = 0; r < R; ++r) buf[q0 + r * (wstep + (wstep >> 4))] = v[g * R + r];
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) buf[fpad(i0 + r * wstep)] = v[g * R + r];
       }
     }
     __syncthreads();
@@ -887,7 +897,7 @@ __device__ __forceinline__ void stockham8(cpx<T>* buf, const cpx<T>* st_tab, boo
 }
 
 template <typename T, int LN, int LL>
-__global__ void __launch_bounds__(256, 2) k_fft_t(const void* in, void* out,  // may alias
+__global__ void __launch_bounds__(256, 3) k_fft_t(const void* in, void* out,  // may alias
                                                int mode, double out_scale, int64_t st, int n,
                                                int64_t hi, int64_t ntiles,
                                                const cpx<T>* __restrict__ tw, int inverse,
@@ -898,12 +908,16 @@ __global__ void __launch_bounds__(256, 2) k_fft_t(const void* in, void* out,  //
   extern __shared__ __align__(16) unsigned char fft_smem[];
   const int hn = n / 2;
   constexpr int bufc = kFftTileSlots;
+  constexpr int NP = NT / 2 + 1;  // bin pairs (k, NT - k) per line of a real transform
   const T osc = (T)out_scale;
   cpx<T>* ts = reinterpret_cast<cpx<T>*>(fft_smem);
-  cpx<T>* const buf0 = ts + NT;
+  cpx<T>* const rtw = ts + NT;               // w^k, k <= NT/2, of the real transforms
+  cpx<T>* const buf0 = rtw + kFftRtwSlots(NT);
   __shared__ double denl[16];
   __shared__ int64_t lbase[16];
   build_r8_twiddles<T, LN>(ts, tw, (mode == FFT_C2C) ? 1 : 2);
+  if (mode != FFT_C2C)
+    for (int k = threadIdx.x; k < NP; k += blockDim.x) rtw[k] = tw[k];
   const bool inv_first = (mode == FFT_C2R) || inverse != 0;
   constexpr int CS = (int)sizeof(cpx<T>);
   const bool lo_lines = st > 1;
@@ -1008,22 +1022,34 @@ __global__ void __launch_bounds__(256, 2) k_fft_t(const void* in, void* out,  //
     __syncthreads();
     cpx<T>* buf = buf0 + b * bufc;
     if (mode == FFT_C2R) {
-      cpx<T> zv[PER];
+      // pair (k, NT-k): Z[k] = E + i O, Z[NT-k] = conj(E - i O) with
+      // E = (X[k] + conj X[NT-k]) / 2, O = conj(w^k) (X[k] - conj X[NT-k]) / 2
+      constexpr int NIT = (NP * L + 255) / 256;
+      cpx<T> z1[NIT], z2[NIT];
 #pragma unroll
-      for (int c = 0; c < PER; ++c) {
+      for (int c = 0; c < NIT; ++c) {
         const int e = tid + c * 256;
-        const int l = e >> LN, k = e & (NT - 1);
-        const cpx<T> a = buf[fpad(l * (hn + 1) + k)], bb = cconjt(buf[fpad(l * (hn + 1) + hn - k)]);
-        const cpx<T> E = {(a.re + bb.re) * T(0.5), (a.im + bb.im) * T(0.5)};
-        cpx<T> w = tw[k];
-        w.im = -w.im;
-        const cpx<T> D = {(a.re - bb.re) * T(0.5), (a.im - bb.im) * T(0.5)};
-        const cpx<T> O = cmulc(D, w);
-        zv[c] = {E.re - O.im, E.im + O.re};
+        const int l = e & (L - 1), k = e >> LL;
+        if (k < NP) {
+          const cpx<T> a = buf[fpad(l * (hn + 1) + k)];
+          const cpx<T> bb = cconjt(buf[fpad(l * (hn + 1) + NT - k)]);
+          const cpx<T> E = {(a.re + bb.re) * T(0.5), (a.im + bb.im) * T(0.5)};
+          const cpx<T> D = {(a.re - bb.re) * T(0.5), (a.im - bb.im) * T(0.5)};
+          const cpx<T> O = cmulc(D, cconjt(rtw[k]));
+          z1[c] = {E.re - O.im, E.im + O.re};
+          z2[c] = {E.re + O.im, O.re - E.im};  // conj(E - i O)
+        }
       }
       __syncthreads();
 #pragma unroll
-      for (int c = 0; c < PER; ++c) buf[fpad(tid + c * 256)] = zv[c];
+      for (int c = 0; c < NIT; ++c) {
+        const int e = tid + c * 256;
+        const int l = e & (L - 1), k = e >> LL;
+        if (k < NP) {
+          buf[fpad((l << LN) + k)] = z1[c];
+          if (k > 0 && k < NT / 2) buf[fpad((l << LN) + NT - k)] = z2[c];
+        }
+      }
       __syncthreads();
     }
     if (inv_first) stockham8<T, LN, LL, true>(buf, ts, lo_lines);
@@ -1048,13 +1074,18 @@ __global__ void __launch_bounds__(256, 2) k_fft_t(const void* in, void* out,  //
       const int64_t kst = tr_n1 ? tr_n1 : 1;
       const int l = tid & (L - 1);
       if (hi0 + l < hi) {
-        for (int k = tid >> LL; k <= hn; k += 256 >> LL) {
-          const cpx<T> a = buf[fpad((l << LN) + (k & (NT - 1)))];
+        // pair (k, NT-k): X[k] = E + w^k O, X[NT-k] = conj(E - w^k O) with
+        // E = (Z[k] + conj Z[NT-k]) / 2, O = -i (Z[k] - conj Z[NT-k]) / 2
+        cpx<T>* xl = Xo + lbase[l];
+        for (int k = tid >> LL; k < NP; k += 256 >> LL) {
+          const cpx<T> a = buf[fpad((l << LN) + k)];
           const cpx<T> bb = cconjt(buf[fpad((l << LN) + ((NT - k) & (NT - 1)))]);
           const cpx<T> E = {(a.re + bb.re) * T(0.5), (a.im + bb.im) * T(0.5)};
           const cpx<T> D = {(a.re - bb.re) * T(0.5), (a.im - bb.im) * T(0.5)};
           const cpx<T> O = {D.im, -D.re};
-          Xo[lbase[l] + kst * k] = cadd(E, cmulc(tw[k], O));
+          const cpx<T> WO = cmulc(rtw[k], O);
+          xl[kst * k] = cadd(E, WO);
+          if (k < NT / 2) xl[kst * (NT - k)] = {E.re - WO.re, WO.im - E.im};
         }
       }
     } else if (mode == FFT_C2R) {
