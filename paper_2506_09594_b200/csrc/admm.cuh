@@ -67,6 +67,8 @@ struct Solver {
   const uint8_t* mask;
   T *l, *lold, *e, *y, *z, *zold, *rhs;
   std::vector<T*> gcur, gnew, lag, X;
+  std::vector<T*> lag2;     // second multiplier buffer of the fused sweep tail
+  bool rhs_ready = false;   // rhs already holds this sweep's L right-hand side
   cpx<T>* spec = nullptr;
   std::vector<cpx<T>*> tw;
   double* lam = nullptr;
@@ -430,15 +432,18 @@ static void lag_updates(Solver<T>& s, const T* x, double mu, bool v4, unsigned g
 template <typename T>
 static void lrta_inputs(Solver<T>& s, const T* x, double mu, bool v4, unsigned grid,
                         cudaStream_t st) {
-  ModePtrs<T> lg{}, xs{};
-  lg.count = xs.count = s.cfg.nmodes;
-  for (int k = 0; k < s.cfg.nmodes; ++k) {
-    lg.p[k] = s.lag[k];
-    xs.p[k] = s.X[k];
-    lg.axis[k] = xs.axis[k] = s.cfg.modes[k];
+  for (int k0 = 0; k0 < s.cfg.nmodes; k0 += 4) {
+    const int cnt = std::min(4, s.cfg.nmodes - k0);
+    ModePtrs<T> lg{}, xs{};
+    lg.count = xs.count = cnt;
+    for (int k = 0; k < cnt; ++k) {
+      lg.p[k] = s.lag[k0 + k];
+      xs.p[k] = s.X[k0 + k];
+      lg.axis[k] = xs.axis[k] = s.cfg.modes[k0 + k];
+    }
+    launch("lrta_input", v4 ? k_lrta_input<T, 4> : k_lrta_input<T, 1>, grid, kRedThreads, 0, st,
+           s.g, x, lg, xs, mu);
   }
-  launch("lrta_input", v4 ? k_lrta_input<T, 4> : k_lrta_input<T, 1>, grid, kRedThreads, 0, st,
-         s.g, x, lg, xs, mu);
 }
 
 template <typename T>
@@ -459,6 +464,10 @@ static int admm_step(Solver<T>& s, double* hout) {
   }
   const bool pure = nm == 1 && s.cfg.modes[0] < 0;
   const bool v4 = line_vec4<T>(g, {s.A, s.B, s.l, s.e, s.y, s.z, s.lold, s.rhs}, s.mask);
+  // fused sweep tail (lag + noise/dual + next rhs in one pass): gradient chain,
+  // <= 4 modes, vector path
+  const bool fuse = !s.onebit() && !pure && nm <= 4 && v4 && !s.lag2.empty();
+  if (!fuse) s.rhs_ready = false;
   const auto rhs_k = v4 ? k_admm_rhs<T, 4> : k_admm_rhs<T, 1>;
   double* part = s.part;
   double* res = s.res;  // device scratch for final reductions
@@ -470,13 +479,14 @@ static int admm_step(Solver<T>& s, double* hout) {
     if (pure) {
       launch("admm_rhs", rhs_k, grid, kRedThreads, 0, st, g, s.A, s.e, s.y, mu, gp, lp, s.l);
     } else {
-      launch("admm_rhs", rhs_k, grid, kRedThreads, 0, st, g, s.A, s.e, s.y, mu, gp, lp, s.rhs);
+      if (!s.rhs_ready)
+        launch("admm_rhs", rhs_k, grid, kRedThreads, 0, st, g, s.A, s.e, s.y, mu, gp, lp, s.rhs);
       if (fft_solve2<T>(s, s.rhs, s.l, st)) return 1;
     }
     tau = 1.0 / (gamma * mu);
     lrta_inputs<T>(s, s.l, mu, v4, grid, st);
     if (low_rank_step<T>(s, tau)) return 2;
-    lag_updates<T>(s, s.l, mu, v4, grid, st);
+    if (!fuse) lag_updates<T>(s, s.l, mu, v4, grid, st);
     // noise and dual updates (solvers.py:239-246)
     const double level = s.cfg.lam / mu;
     const int structure = s.cfg.kind == 1 ? 3 : s.cfg.structure;
@@ -502,11 +512,43 @@ static int admm_step(Solver<T>& s, double* hout) {
     case 2: TR_ND2(K, 2); break;            \
     default: TR_ND2(K, 3); break;           \
   }
-    TR_PEN_DISPATCH(s.cfg.psi.kind, TR_ND)
+    if (fuse) {
+      ModePtrs<T> gn{}, go{}, lw{};
+      gn.count = go.count = lw.count = nm;
+      for (int k = 0; k < nm; ++k) {
+        gn.p[k] = s.gnew[k];
+        go.p[k] = s.gcur[k];
+        lw.p[k] = s.lag2[k];
+        gn.axis[k] = go.axis[k] = lw.axis[k] = s.cfg.modes[k];
+      }
+      const double mu_next = std::min(s.cfg.mu_max, s.cfg.growth * mu);
+#define TR_ST2(K, S)                                                                            \
+  launch("sweep_tail", k_sweep_tail<T, K, S>, grid, kRedThreads, 0, st, g, s.A, s.mask,         \
+         (const T*)s.l, (const T*)s.lold, s.e, s.y, gn, go, lp, lw, mu, mu_next, q0, q1, level, \
+         (const double*)s.scale, s.rhs, part)
+#define TR_ST(K)                 \
+  switch (structure) {           \
+    case 0: TR_ST2(K, 0); break; \
+    case 1: TR_ST2(K, 1); break; \
+    case 2: TR_ST2(K, 2); break; \
+    default: TR_ST2(K, 3); break; \
+  }
+      TR_PEN_DISPATCH(s.cfg.psi.kind, TR_ST)
+#undef TR_ST
+#undef TR_ST2
+      // partial slots: 5 per mode (4 slots) then the 7 noise values -> res[96..122]
+      launch("final_reduce", k_final_reduce, 1, 256, 0, st, (const double*)part, (int)rb, 27,
+             0b0010101u << 20 | 0b00101u | 0b00101u << 5 | 0b00101u << 10 | 0b00101u << 15,
+             res + 96);
+      for (int k = 0; k < nm; ++k) std::swap(s.lag[k], s.lag2[k]);
+      s.rhs_ready = true;
+    } else {
+      TR_PEN_DISPATCH(s.cfg.psi.kind, TR_ND)
+      launch("final_reduce", k_final_reduce, 1, 256, 0, st, (const double*)part, (int)rb, 7,
+             0b0010101u, res + 64);
+    }
 #undef TR_ND
 #undef TR_ND2
-    launch("final_reduce", k_final_reduce, 1, 256, 0, st, (const double*)part, (int)rb, 7,
-           0b0010101u, res + 64);
   } else {
     // one-bit (onebit.py:171-192)
     const bool robust = s.cfg.kind == 3;
@@ -541,14 +583,16 @@ static int admm_step(Solver<T>& s, double* hout) {
   TR_CUDA(cudaMemcpyAsync(s.hres, res, 128 * sizeof(double), cudaMemcpyDeviceToHost, st));
   TR_CUDA(cudaStreamSynchronize(st));
   const double* h = s.hres;
+  const double* hl = fuse ? h + 96 : h;          // per-mode multiplier residuals
+  const double* hn = fuse ? h + 96 + 20 : h + 64;  // noise / dual residuals
   for (int i = 0; i < R_NOUT; ++i) hout[i] = 0.0;
   double grad = 0, dg = 0, dgf = 0, gradf = 0, lagn = 0;
   for (int k = 0; k < nm; ++k) {
-    grad = fmax(grad, h[5 * k + 0]);
-    gradf = fmax(gradf, sqrt(h[5 * k + 1]));
-    dg = fmax(dg, h[5 * k + 2]);
-    dgf = fmax(dgf, sqrt(h[5 * k + 3]));
-    lagn = fmax(lagn, sqrt(h[5 * k + 4]));
+    grad = fmax(grad, hl[5 * k + 0]);
+    gradf = fmax(gradf, sqrt(hl[5 * k + 1]));
+    dg = fmax(dg, hl[5 * k + 2]);
+    dgf = fmax(dgf, sqrt(hl[5 * k + 3]));
+    lagn = fmax(lagn, sqrt(hl[5 * k + 4]));
   }
   hout[R_GRAD] = grad;
   hout[R_GRAD_FRO] = gradf;
@@ -557,13 +601,13 @@ static int admm_step(Solver<T>& s, double* hout) {
   hout[R_LAG_NORM] = lagn;
   hout[R_MU] = mu;
   if (!s.onebit()) {
-    hout[R_DL] = h[64];
-    hout[R_DL_FRO] = sqrt(h[65]);
-    hout[R_DE] = h[66];
-    hout[R_DE_FRO] = sqrt(h[67]);
-    hout[R_FIT] = h[68];
-    hout[R_FIT_FRO] = sqrt(h[69]);
-    hout[R_Y_NORM] = sqrt(h[70]);
+    hout[R_DL] = hn[0];
+    hout[R_DL_FRO] = sqrt(hn[1]);
+    hout[R_DE] = hn[2];
+    hout[R_DE_FRO] = sqrt(hn[3]);
+    hout[R_FIT] = hn[4];
+    hout[R_FIT_FRO] = sqrt(hn[5]);
+    hout[R_Y_NORM] = sqrt(hn[6]);
   } else {
     hout[R_REL_DL] = sqrt(h[80]) / fmax(sqrt(h[81]), 1e-30);
     hout[R_DL] = h[82];
@@ -639,6 +683,9 @@ static int admm_create(const AdmmConfig& cfg, int order, const int64_t* dims, co
     s->lag.push_back(s->template alloc<T>(N));
     s->X.push_back(s->template alloc<T>(N));
   }
+  // second multiplier buffers for the fused sweep tail (gradient chain, <= 4 modes)
+  if (cfg.kind < 2 && nm <= 4 && cfg.modes[0] >= 0 && getenv("TR_NO_FUSE") == nullptr)
+    for (int k = 0; k < nm; ++k) s->lag2.push_back(s->template alloc<T>(N));
   s->spec = s->template alloc<cpx<T>>(N);
   int64_t lam_total = 0;
   for (int i = 0; i < order; ++i) {
@@ -648,7 +695,7 @@ static int admm_create(const AdmmConfig& cfg, int order, const int64_t* dims, co
   s->lam = s->template alloc<double>(lam_total);
   s->scale = s->template alloc<double>(std::max<int64_t>(dims[0] * dims[1], N / (dims[0] * dims[1])));
   s->red_blocks = grid_for<T>(N);
-  s->part = s->template alloc<double>(s->red_blocks * 20);  // up to 4 modes x 5 partials
+  s->part = s->template alloc<double>(s->red_blocks * 27);  // fused tail: 4 x 5 + 7 partials
   s->res = s->template alloc<double>(128);
   for (void* p : s->allocs)
     if (!p) {

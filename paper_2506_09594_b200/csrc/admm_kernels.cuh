@@ -74,6 +74,25 @@ __device__ __forceinline__ Vec<T, V> ldv(const T* p) {
   return r;
 }
 
+// read-only variant (ld.global.nc): the compiler may schedule these loads
+// across the kernel's stores, which raises memory-level parallelism
+template <typename T, int V>
+__device__ __forceinline__ Vec<T, V> ldv_nc(const T* p) {
+  Vec<T, V> r;
+  if constexpr (V == 4 && sizeof(T) == 4) {
+    const float4 f = __ldg(reinterpret_cast<const float4*>(p));
+    r.x[0] = f.x; r.x[1] = f.y; r.x[2] = f.z; r.x[3] = f.w;
+  } else if constexpr (V == 4 && sizeof(T) == 8) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    r.x[0] = a.x; r.x[1] = a.y; r.x[2] = b.x; r.x[3] = b.y;
+  } else {
+#pragma unroll
+    for (int j = 0; j < V; ++j) r.x[j] = __ldg(p + j);
+  }
+  return r;
+}
+
 template <typename T, int V>
 __device__ __forceinline__ void stv(T* p, const T (&v)[V]) {
   if constexpr (V == 4 && sizeof(T) == 4) {
@@ -99,22 +118,48 @@ __device__ __forceinline__ void ld_mask(const uint8_t* p, bool (&m)[V]) {
   }
 }
 
-// Walk every V-element chunk of every axis-0 line: f(line, i0).  Long lines
-// are split across the block's threads; short lines pack several per pass.
+// A line (axis-0 fiber) and its coordinates along axes 1..d-1.
+struct LineCo {
+  int64_t line;
+  int co[kMaxOrder];
+};
+
+// Walk every V-element chunk of every axis-0 line: f(lc, i0).  Long lines are
+// split across the block's threads, and each block takes a contiguous range of
+// an enumeration of the lines in which the LAST axis runs fastest: a line's
+// neighbours along the outer axes are then this block's previous / next lines
+// or lines that adjacent blocks touch at the same time, so the stencil
+// re-reads hit L2.  Short lines pack several per pass.
 template <int V, typename F>
 __device__ __forceinline__ void for_each_chunk(const Geom& g, F&& f) {
   const int64_t n0 = g.dims[0], lines = g.N / n0;
   const int cpl = (int)(n0 / V);
+  LineCo lc;
   if (cpl >= (int)blockDim.x) {
-    for (int64_t line = blockIdx.x; line < lines; line += gridDim.x)
-      for (int c = threadIdx.x; c < cpl; c += blockDim.x) f(line, (int64_t)c * V);
+    const int64_t per = (lines + gridDim.x - 1) / gridDim.x;
+    const int64_t j0 = (int64_t)blockIdx.x * per, j1 = min(lines, j0 + per);
+    for (int64_t j = j0; j < j1; ++j) {
+      int64_t r = j, line = 0;
+      for (int a = g.d - 1; a >= 1; --a) {
+        const int64_t n = g.dims[a];
+        const int64_t q = (r < (1ll << 31) && n < (1ll << 31))
+                              ? (int64_t)((uint32_t)r / (uint32_t)n) : r / n;
+        lc.co[a] = (int)(r - q * n);
+        line += (r - q * n) * g.lst[a];
+        r = q;
+      }
+      lc.line = line;
+      for (int c = threadIdx.x; c < cpl; c += blockDim.x) f(lc, (int64_t)c * V);
+    }
   } else {
     const int lpi = (int)blockDim.x / cpl;
     const int sub = (int)threadIdx.x / cpl, c = (int)threadIdx.x - sub * cpl;
     if (sub >= lpi) return;
     for (int64_t l0 = (int64_t)blockIdx.x * lpi; l0 < lines; l0 += (int64_t)gridDim.x * lpi) {
-      const int64_t line = l0 + sub;
-      if (line < lines) f(line, (int64_t)c * V);
+      lc.line = l0 + sub;
+      if (lc.line >= lines) continue;
+      for (int a = 1; a < g.d; ++a) lc.co[a] = (int)line_coord(g, lc.line, a);
+      f(lc, (int64_t)c * V);
     }
   }
 }
@@ -122,7 +167,7 @@ __device__ __forceinline__ void for_each_chunk(const Geom& g, F&& f) {
 // forward difference D_a x at the V elements of a chunk (x already loaded);
 // a < 0: identity chain
 template <typename T, int V>
-__device__ __forceinline__ void fwd_diff(const Geom& g, const T* x, int a, int64_t line,
+__device__ __forceinline__ void fwd_diff(const Geom& g, const T* x, int a, const LineCo& lc,
                                          int64_t base, int64_t i0, const Vec<T, V>& xv,
                                          T (&out)[V]) {
   const int64_t n0 = g.dims[0];
@@ -130,13 +175,13 @@ __device__ __forceinline__ void fwd_diff(const Geom& g, const T* x, int a, int64
 #pragma unroll
     for (int j = 0; j < V; ++j) out[j] = xv.x[j];
   } else if (a == 0) {
-    const T last = x[base + (i0 + V < n0 ? i0 + V : 0)];
+    const T last = __ldg(x + base + (i0 + V < n0 ? i0 + V : 0));
 #pragma unroll
     for (int j = 0; j < V; ++j) out[j] = (j + 1 < V ? xv.x[j + 1] : last) - xv.x[j];
   } else {
     int64_t pv, nx;
-    axis_offsets(g, a, line_coord(g, line, a), pv, nx);
-    const Vec<T, V> xn = ldv<T, V>(x + base + i0 + nx);
+    axis_offsets(g, a, lc.co[a], pv, nx);
+    const Vec<T, V> xn = ldv_nc<T, V>(x + base + i0 + nx);
 #pragma unroll
     for (int j = 0; j < V; ++j) out[j] = xn.x[j] - xv.x[j];
   }
@@ -185,7 +230,8 @@ __global__ void __launch_bounds__(kRedThreads) k_admm_rhs(Geom g, const T* __res
   const int64_t n0 = g.dims[0];
   const T imu = (T)(1.0 / mu);
   const bool pure = gm.count == 1 && gm.axis[0] < 0;
-  for_each_chunk<V>(g, [&](int64_t line, int64_t i0) {
+  for_each_chunk<V>(g, [&](const LineCo& lc, int64_t i0) {
+    const int64_t line = lc.line;
     const int64_t base = line * n0, i = base + i0;
     const Vec<T, V> av = ldv<T, V>(A + i), yv = ldv<T, V>(y + i);
     Vec<T, V> bv;
@@ -215,7 +261,7 @@ __global__ void __launch_bounds__(kRedThreads) k_admm_rhs(Geom g, const T* __res
           for (int j = 1; j < V; ++j) gp[j] = gi[j - 1];
         } else {
           int64_t pv, nx;
-          axis_offsets(g, a, line_coord(g, line, a), pv, nx);
+          axis_offsets(g, a, lc.co[a], pv, nx);
           const Vec<T, V> gq = ldv<T, V>(gm.p[k] + i + pv), lq = ldv<T, V>(lag.p[k] + i + pv);
 #pragma unroll
           for (int j = 0; j < V; ++j) gp[j] = gq.x[j] - lq.x[j] * imu;
@@ -229,25 +275,45 @@ __global__ void __launch_bounds__(kRedThreads) k_admm_rhs(Geom g, const T* __res
 }
 
 // LRTA inputs of every mode (one pass over L): X_k = D_k L + lag_k / mu
-// (identity chain: L + lag / mu)
+// (identity chain: L + lag / mu) for up to 4 modes (the host launches groups).
+// All loads of a chunk are issued before its stores.
 template <typename T, int V>
 __global__ void __launch_bounds__(kRedThreads) k_lrta_input(Geom g, const T* __restrict__ l,
                                                             ModePtrs<T> lag, ModePtrs<T> X,
                                                             double mu) {
+  constexpr int MM = 4;
   const T imu = (T)(1.0 / mu);
   const int64_t n0 = g.dims[0];
-  for_each_chunk<V>(g, [&](int64_t line, int64_t i0) {
-    const int64_t base = line * n0, i = base + i0;
-    const Vec<T, V> lv = ldv<T, V>(l + i);
+  const int nm = lag.count;
+  for_each_chunk<V>(g, [&](const LineCo& lc, int64_t i0) {
+    const int64_t base = lc.line * n0, i = base + i0;
+    const Vec<T, V> lv = ldv_nc<T, V>(l + i);
+    Vec<T, V> mv[MM], xn[MM];
 #pragma unroll
-    for (int k = 0; k < kMaxOrder; ++k) {
-      if (k < lag.count) {
-        T gl[V];
-        fwd_diff<T, V>(g, l, lag.axis[k], line, base, i0, lv, gl);
-        const Vec<T, V> mv = ldv<T, V>(lag.p[k] + i);
+    for (int k = 0; k < MM; ++k) {
+      if (k < nm) {
+        const int a = lag.axis[k];
+        mv[k] = ldv_nc<T, V>(lag.p[k] + i);
+        if (a == 0) {
+          xn[k].x[0] = __ldg(l + base + (i0 + V < n0 ? i0 + V : 0));
+        } else if (a > 0) {
+          int64_t pv, nx;
+          axis_offsets(g, a, lc.co[a], pv, nx);
+          xn[k] = ldv_nc<T, V>(l + i + nx);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < MM; ++k) {
+      if (k < nm) {
+        const int a = lag.axis[k];
         T o[V];
 #pragma unroll
-        for (int j = 0; j < V; ++j) o[j] = gl[j] + mv.x[j] * imu;
+        for (int j = 0; j < V; ++j) {
+          const T gl = a < 0 ? lv.x[j]
+                             : (a == 0 ? (j + 1 < V ? lv.x[j + 1] : xn[k].x[0]) : xn[k].x[j]) - lv.x[j];
+          o[j] = gl + mv[k].x[j] * imu;
+        }
         stv<T, V>(X.p[k] + i, o);
       }
     }
@@ -268,13 +334,14 @@ __global__ void __launch_bounds__(kRedThreads) k_lag_update(Geom g, const T* __r
   for (int q = 0; q < 5 * NM; ++q) v[q] = 0.0;
   const int64_t n0 = g.dims[0];
   const T tmu = (T)mu;
-  for_each_chunk<V>(g, [&](int64_t line, int64_t i0) {
+  for_each_chunk<V>(g, [&](const LineCo& lc, int64_t i0) {
+    const int64_t line = lc.line;
     const int64_t base = line * n0, i = base + i0;
     const Vec<T, V> lv = ldv<T, V>(l + i);
 #pragma unroll
     for (int k = 0; k < NM; ++k) {
       T gl[V];
-      fwd_diff<T, V>(g, l, lag.axis[k], line, base, i0, lv, gl);
+      fwd_diff<T, V>(g, l, lag.axis[k], lc, base, i0, lv, gl);
       const Vec<T, V> gn = ldv<T, V>(gnew.p[k] + i), go = ldv<T, V>(gold.p[k] + i);
       const Vec<T, V> lo = ldv<T, V>(lag.p[k] + i);
       T ln[V];
@@ -378,7 +445,8 @@ __global__ void __launch_bounds__(kRedThreads) k_noise_dual(Geom g, const T* __r
   const int64_t face = g.dims[0] * g.dims[1];
   const int64_t n0 = g.dims[0];
   const T tmu = (T)mu, tlev = (T)level, tp0 = (T)p0, timu = (T)(1.0 / mu);
-  for_each_chunk<V>(g, [&](int64_t line, int64_t i0) {
+  for_each_chunk<V>(g, [&](const LineCo& lc, int64_t i0) {
+    const int64_t line = lc.line;
     const int64_t i = line * n0 + i0;
     const Vec<T, V> mv = ldv<T, V>(mobs + i), lv = ldv<T, V>(l + i), yv = ldv<T, V>(y + i);
     const Vec<T, V> ev = ldv<T, V>(e + i), ov = ldv<T, V>(lold + i);
@@ -419,6 +487,153 @@ __global__ void __launch_bounds__(kRedThreads) k_noise_dual(Geom g, const T* __r
 #pragma unroll
   for (int q = 0; q < 7; ++q) vd[q] = (double)v[q];
   block_partials<7>(vd, 0b0010101u, red, part);
+}
+
+// Tail of ADMM sweep t and head of sweep t+1 in ONE pass (solvers.py:244-248,
+// then 230-232 of the next iteration), for the gradient chain with <= 4 modes:
+//   lag'_k = lag_k + mu (D_k L - G_k)          written to lagw_k (double buffer:
+//                                              neighbours still read lag_k)
+//   E', Y'  exactly as k_noise_dual
+//   rhs'    = A - E' + Y'/mu' + sum_k D_k^T (G_k - lag'_k / mu'),  mu' = min(mu_max, growth mu)
+// D_k^T at i needs lag'_k at ip = i - e_k; it is recomputed from lag_k, G_k, L
+// at ip with the very expression the owner of ip evaluates, so rhs' is
+// bit-identical to k_admm_rhs of the next sweep.  Partials per block: 5 per
+// mode slot (k_lag_update's, 4 slots) then the 7 of k_noise_dual.
+template <typename T, int KIND, int STRUCT>
+__global__ void __launch_bounds__(kRedThreads, 1) k_sweep_tail(
+    Geom g, const T* __restrict__ mobs, const uint8_t* __restrict__ mask, const T* __restrict__ l,
+    const T* __restrict__ lold, T* __restrict__ e, T* __restrict__ y, ModePtrs<T> gn, ModePtrs<T> go,
+    ModePtrs<T> lag, ModePtrs<T> lagw, double mu, double mu_next, double p0, double p1,
+    double level, const double* __restrict__ scale, T* __restrict__ rhs,
+    double* __restrict__ part) {
+  constexpr int V = 4, MM = 4;  // mode slots
+  __shared__ double red[32];
+  // per-thread partials in T (sums over a few hundred elements), per-block fp64
+  T vl[5 * MM], vn[7];
+#pragma unroll
+  for (int q = 0; q < 5 * MM; ++q) vl[q] = T(0);
+#pragma unroll
+  for (int q = 0; q < 7; ++q) vn[q] = T(0);
+  const int nm = gn.count;
+  const int64_t n0 = g.dims[0], face = g.dims[0] * g.dims[1];
+  const T tmu = (T)mu, tlev = (T)level, tp0 = (T)p0, timu = (T)(1.0 / mu);
+  const T imu2 = (T)(1.0 / mu_next);
+  for_each_chunk<V>(g, [&](const LineCo& lc, int64_t i0) {
+    const int64_t base = lc.line * n0, i = base + i0;
+    // ---- every load of the chunk first (memory-level parallelism) ----
+    const Vec<T, V> lv = ldv_nc<T, V>(l + i), mv = ldv_nc<T, V>(mobs + i);
+    const Vec<T, V> ov = ldv_nc<T, V>(lold + i);
+    const Vec<T, V> yv = ldv<T, V>(y + i), ev = ldv<T, V>(e + i);
+    bool obs[V];
+    ld_mask<V>(mask + i, obs);
+    Vec<T, V> gnv[MM], gov[MM], lgv[MM], lnx[MM], lpv[MM], gpv[MM], mpv[MM];
+#pragma unroll
+    for (int k = 0; k < MM; ++k) {
+      if (k < nm) {
+        const int a = lag.axis[k];
+        gnv[k] = ldv_nc<T, V>(gn.p[k] + i);
+        gov[k] = ldv_nc<T, V>(go.p[k] + i);
+        lgv[k] = ldv_nc<T, V>(lag.p[k] + i);
+        if (a == 0) {
+          const int64_t inext = base + (i0 + V < n0 ? i0 + V : 0);
+          const int64_t ip = base + (i0 > 0 ? i0 - 1 : n0 - 1);
+          lnx[k].x[0] = __ldg(l + inext);
+          lpv[k].x[0] = __ldg(l + ip);
+          gpv[k].x[0] = __ldg(gn.p[k] + ip);
+          mpv[k].x[0] = __ldg(lag.p[k] + ip);
+        } else {
+          int64_t pv, nx;
+          axis_offsets(g, a, lc.co[a], pv, nx);
+          lnx[k] = ldv_nc<T, V>(l + i + nx);
+          lpv[k] = ldv_nc<T, V>(l + i + pv);
+          gpv[k] = ldv_nc<T, V>(gn.p[k] + i + pv);
+          mpv[k] = ldv_nc<T, V>(lag.p[k] + i + pv);
+        }
+      }
+    }
+    // ---- noise and dual (k_noise_dual) ----
+    T en[V], yn[V], acc[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const T mi = mv.x[j], li = lv.x[j], yi = yv.x[j];
+      const T h = mi - li + yi * timu;
+      T ej;
+      if (!obs[j]) {
+        ej = h;
+      } else if (STRUCT == 3) {
+        ej = T(0);
+      } else if (STRUCT == 0) {
+        ej = prox_t<KIND, T>(tp0, p0, p1, tlev, level, h);
+      } else {
+        const double sc = STRUCT == 1 ? scale[(i + j) % face] : scale[(i + j) / face];
+        ej = (T)((double)h * sc);
+      }
+      const T fit = mi - li - ej;
+      en[j] = ej;
+      yn[j] = yi + tmu * fit;
+      const T dl = li - ov.x[j], de = ej - ev.x[j];
+      vn[0] = fmax(vn[0], fabs(dl));
+      vn[1] += dl * dl;
+      vn[2] = fmax(vn[2], fabs(de));
+      vn[3] += de * de;
+      vn[4] = fmax(vn[4], fabs(fit));
+      vn[5] += fit * fit;
+      vn[6] += yn[j] * yn[j];
+      acc[j] = (mi - ej) + yn[j] * imu2;  // b' = A - E' + Y' / mu'
+    }
+    stv<T, V>(e + i, en);
+    stv<T, V>(y + i, yn);
+    // ---- multipliers (k_lag_update) and the next rhs (k_admm_rhs) ----
+#pragma unroll
+    for (int k = 0; k < MM; ++k) {
+      if (k < nm) {
+        const int a = lag.axis[k];
+        T gl[V], ln[V], gi[V], gp[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j)  // D_a L (as fwd_diff)
+          gl[j] = (a == 0 ? (j + 1 < V ? lv.x[j + 1] : lnx[k].x[0]) : lnx[k].x[j]) - lv.x[j];
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          const T gap = gl[j] - gnv[k].x[j];
+          ln[j] = lgv[k].x[j] + tmu * gap;
+          const T dg = gnv[k].x[j] - gov[k].x[j];
+          vl[5 * k + 0] = fmax(vl[5 * k + 0], fabs(gap));
+          vl[5 * k + 1] += gap * gap;
+          vl[5 * k + 2] = fmax(vl[5 * k + 2], fabs(dg));
+          vl[5 * k + 3] += dg * dg;
+          vl[5 * k + 4] += ln[j] * ln[j];
+          gi[j] = gnv[k].x[j] - ln[j] * imu2;
+        }
+        stv<T, V>(lagw.p[k] + i, ln);
+        // lag' at ip = i - e_a, with its owner's expression (D_a L at ip = L[i] - L[ip])
+        if (a == 0) {
+          const T gap = (lv.x[0] - lpv[k].x[0]) - gpv[k].x[0];
+          const T lnp = mpv[k].x[0] + tmu * gap;
+          gp[0] = gpv[k].x[0] - lnp * imu2;
+#pragma unroll
+          for (int j = 1; j < V; ++j) gp[j] = gi[j - 1];
+        } else {
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            const T gap = (lv.x[j] - lpv[k].x[j]) - gpv[k].x[j];
+            const T lnp = mpv[k].x[j] + tmu * gap;
+            gp[j] = gpv[k].x[j] - lnp * imu2;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[j] += gp[j] - gi[j];
+      }
+    }
+    stv<T, V>(rhs + i, acc);
+  });
+  double vd[27];
+#pragma unroll
+  for (int q = 0; q < 20; ++q) vd[q] = (double)vl[q];
+#pragma unroll
+  for (int q = 0; q < 7; ++q) vd[20 + q] = (double)vn[q];
+  constexpr unsigned kMax = 0b00101u | (0b00101u << 5) | (0b00101u << 10) | (0b00101u << 15) |
+                            (0b0010101u << 20);
+  block_partials<27>(vd, kMax, red, part);
 }
 
 // one-bit data-fit update (onebit.py:128-138, 172-180):
