@@ -252,6 +252,22 @@ __device__ __forceinline__ void jacobi_cs(double app, double aqq, double apq, do
   s = t * c;
 }
 
+// Same rotation with the tangent formed in fp32 (MUFU rcp/sqrt) and c, s
+// completed in fp64 from it: the rotation stays exactly orthogonal in fp64;
+// only the annihilation of a_pq is fp32-accurate, which the following sweeps
+// absorb.  Shortens the serial latency chain of a Jacobi round.
+__device__ __forceinline__ void jacobi_cs_fast(double app, double aqq, double apq, double& c,
+                                               double& s) {
+  const double r = (aqq - app) * 0.5 * fast_rcp(apq);
+  const float rf = (float)r;
+  float tf;
+  if (fabsf(rf) > 1e15f) tf = 0.5f / rf;
+  else tf = copysignf(1.0f, rf) / (fabsf(rf) + sqrtf(1.0f + rf * rf));
+  const double t = (double)tf;
+  c = fast_rsqrt(1.0 + t * t);
+  s = t * c;
+}
+
 // Krylov piece normalisation (sketch.py:257-258): piece = blk / ||blk||_F.
 template <typename T>
 __global__ void __launch_bounds__(1024) k_normalize_piece(double* __restrict__ kslot,
@@ -406,80 +422,170 @@ __global__ void __launch_bounds__(512) k_ritz(const double* __restrict__ Mfull, 
     if (a != b) diag2 += A[a + ld * b] * A[a + ld * b];
   }
   const double mnorm = sqrt(block_sum(diag2, red));
-  for (int sweep = 0; sweep < 40 && ne >= 2; ++sweep) {
-    for (int rnd = 0; rnd < ne - 1; ++rnd) {
-      const int npairs = ne / 2;
-      if (threadIdx.x < npairs) {
-        int p = rr_player(threadIdx.x, rnd, ne), q = rr_player(ne - 1 - threadIdx.x, rnd, ne);
-        if (p > q) { const int t = p; p = q; q = t; }
-        double c = 1.0, sn = 0.0;
-        if (q < n) {
-          const double apq = A[p + ld * q];
-          const double app = A[p + ld * p], aqq = A[q + ld * q];
-          // skip pairs already decoupled to working precision, relative to the
-          // pair and to ||M|| (rotating rounding noise never converges)
-          if (fabs(apq) > 1e-15 * sqrt(fabs(app * aqq)) && fabs(apq) > 1e-16 * mnorm) {
-            rot_any = 1;
-            jacobi_cs(app, aqq, apq, c, sn);
-          }
-        }
-        pp[threadIdx.x] = p;
-        pq[threadIdx.x] = q;
-        cs_c[threadIdx.x] = c;
-        cs_s[threadIdx.x] = sn;
-      }
-      __syncthreads();
-      // one pass per round: the rotations of a round act on disjoint index
-      // pairs, so J^T A J splits into independent 2x2 blocks
-      // B'(k1,k2) = J_k1^T B(k1,k2) J_k2 (upper blocks, mirrored), and Q <- Q J
-      // row by row; only the live n x n part is touched.
-      for (int e = threadIdx.x; e < npairs * npairs + npairs * n; e += blockDim.x) {
-        if (e < npairs * npairs) {
-          const int k1 = e / npairs, k2 = e - k1 * npairs;
-          if (k1 > k2) continue;
-          const double s1 = cs_s[k1], s2 = cs_s[k2];
-          if (s1 == 0.0 && s2 == 0.0) continue;
-          const double c1 = cs_c[k1], c2 = cs_c[k2];
-          const int p1 = pp[k1], q1 = pq[k1], p2 = pp[k2], q2 = pq[k2];
-          const double a = A[p1 + ld * p2], b = A[p1 + ld * q2];
-          const double c = A[q1 + ld * p2], d = A[q1 + ld * q2];
-          // columns (B J2), then rows (J1^T .)
-          const double ap = c2 * a - s2 * b, bq = s2 * a + c2 * b;
-          const double cp = c2 * c - s2 * d, dq = s2 * c + c2 * d;
-          const double npp = c1 * ap - s1 * cp, npq = c1 * bq - s1 * dq;
-          const double nqp = s1 * ap + c1 * cp, nqq = s1 * bq + c1 * dq;
-          A[p1 + ld * p2] = npp;
-          A[p1 + ld * q2] = npq;
-          A[q1 + ld * p2] = nqp;
-          A[q1 + ld * q2] = nqq;
-          if (k1 != k2) {
-            A[p2 + ld * p1] = npp;
-            A[q2 + ld * p1] = npq;
-            A[p2 + ld * q1] = nqp;
-            A[q2 + ld * q1] = nqq;
-          }
-        } else {
-          const int e2 = e - npairs * npairs;
-          const int k = e2 / n, i = e2 - k * n;
-          const double sn = cs_s[k];
-          if (sn == 0.0) continue;
-          const double c = cs_c[k];
-          const int p = pp[k], q = pq[k];
-          const double qp = Q[i + ld * p], qq = Q[i + ld * q];
-          Q[i + ld * p] = c * qp - sn * qq;
-          Q[i + ld * q] = sn * qp + c * qq;
-        }
-      }
-      __syncthreads();
+  if (ne <= 32 && blockDim.x >= 256) {
+    // n <= 32: fixed roles, decoded once -- thread t owns the 2x2 block
+    // (t >> 4, t & 15) of the round's J^T A J and the Q row pairs
+    // (row t & 31, pairs (t >> 5) and (t >> 5) + 8); two barriers per round.
+    const int npairs = ne / 2;
+    const int t = threadIdx.x;
+    __shared__ unsigned char sched[31][16][2];  // round-robin pairs (p < q) of every round
+    for (int e = t; e < (ne - 1) * npairs; e += blockDim.x) {
+      const int rnd = e / npairs, k = e - rnd * npairs;
+      int p = rr_player(k, rnd, ne), q = rr_player(ne - 1 - k, rnd, ne);
+      if (p > q) { const int tt = p; p = q; q = tt; }
+      sched[rnd][k][0] = (unsigned char)p;
+      sched[rnd][k][1] = (unsigned char)q;
     }
-    // converged once a whole sweep needed no rotation (every |a_pq| is below
-    // 1e-15 sqrt(|a_pp a_qq|), the classical Jacobi stopping rule)
-    const int any = rot_any;
     __syncthreads();
-    if (threadIdx.x == 0) rot_any = 0;
-    __syncthreads();
-    if (threadIdx.x == 0) atomicAdd(&g_dbg[0], 1);  // ritz sweeps
-    if (!any) break;
+    const double mthr = 1e-16 * mnorm;
+    const int bk1 = t >> 4, bk2 = t & 15;
+    const bool blk = t < 256 && bk1 <= bk2 && bk2 < npairs;
+    const int qi = t & 31, qk0 = (t >> 5) & 7;
+    const bool qrow = t < 256 && qi < n;
+    for (int sweep = 0; sweep < 40 && ne >= 2; ++sweep) {
+      for (int rnd = 0; rnd < ne - 1; ++rnd) {
+        if (t < npairs) {
+          const int p = sched[rnd][t][0], q = sched[rnd][t][1];
+          double c = 1.0, sn = 0.0;
+          if (q < n) {
+            const double apq = A[p + ld * q];
+            const double app = A[p + ld * p], aqq = A[q + ld * q];
+            // |apq| > 1e-15 sqrt|app aqq|  <=>  apq^2 > 1e-30 |app aqq|
+            if (apq * apq > 1e-30 * fabs(app * aqq) && fabs(apq) > mthr) {
+              rot_any = 1;
+              jacobi_cs_fast(app, aqq, apq, c, sn);
+            }
+          }
+          pp[t] = p;
+          pq[t] = q;
+          cs_c[t] = c;
+          cs_s[t] = sn;
+        }
+        __syncthreads();
+        if (blk) {
+          const double s1 = cs_s[bk1], s2 = cs_s[bk2];
+          if (s1 != 0.0 || s2 != 0.0) {
+            const double c1 = cs_c[bk1], c2 = cs_c[bk2];
+            const int p1 = pp[bk1], q1 = pq[bk1], p2 = pp[bk2], q2 = pq[bk2];
+            const double a = A[p1 + ld * p2], b = A[p1 + ld * q2];
+            const double c = A[q1 + ld * p2], d = A[q1 + ld * q2];
+            const double ap = c2 * a - s2 * b, bq = s2 * a + c2 * b;
+            const double cp = c2 * c - s2 * d, dq = s2 * c + c2 * d;
+            const double npp = c1 * ap - s1 * cp, npq = c1 * bq - s1 * dq;
+            const double nqp = s1 * ap + c1 * cp, nqq = s1 * bq + c1 * dq;
+            A[p1 + ld * p2] = npp;
+            A[p1 + ld * q2] = npq;
+            A[q1 + ld * p2] = nqp;
+            A[q1 + ld * q2] = nqq;
+            if (bk1 != bk2) {
+              A[p2 + ld * p1] = npp;
+              A[q2 + ld * p1] = npq;
+              A[p2 + ld * q1] = nqp;
+              A[q2 + ld * q1] = nqq;
+            }
+          }
+        }
+        if (qrow) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int k = qk0 + 8 * u;
+            if (k < npairs) {
+              const double sn = cs_s[k];
+              if (sn != 0.0) {
+                const double c = cs_c[k];
+                const int p = pp[k], q = pq[k];
+                const double qp = Q[qi + ld * p], qq = Q[qi + ld * q];
+                Q[qi + ld * p] = c * qp - sn * qq;
+                Q[qi + ld * q] = sn * qp + c * qq;
+              }
+            }
+          }
+        }
+        __syncthreads();
+      }
+      const int any = rot_any;
+      __syncthreads();
+      if (threadIdx.x == 0) rot_any = 0;
+      __syncthreads();
+      if (threadIdx.x == 0) atomicAdd(&g_dbg[0], 1);  // ritz sweeps
+      if (!any) break;
+    }
+  } else {
+    for (int sweep = 0; sweep < 40 && ne >= 2; ++sweep) {
+      for (int rnd = 0; rnd < ne - 1; ++rnd) {
+        const int npairs = ne / 2;
+        if (threadIdx.x < npairs) {
+          int p = rr_player(threadIdx.x, rnd, ne), q = rr_player(ne - 1 - threadIdx.x, rnd, ne);
+          if (p > q) { const int t = p; p = q; q = t; }
+          double c = 1.0, sn = 0.0;
+          if (q < n) {
+            const double apq = A[p + ld * q];
+            const double app = A[p + ld * p], aqq = A[q + ld * q];
+            // skip pairs already decoupled to working precision, relative to the
+            // pair and to ||M|| (rotating rounding noise never converges)
+            if (fabs(apq) > 1e-15 * sqrt(fabs(app * aqq)) && fabs(apq) > 1e-16 * mnorm) {
+              rot_any = 1;
+              jacobi_cs(app, aqq, apq, c, sn);
+            }
+          }
+          pp[threadIdx.x] = p;
+          pq[threadIdx.x] = q;
+          cs_c[threadIdx.x] = c;
+          cs_s[threadIdx.x] = sn;
+        }
+        __syncthreads();
+        // one pass per round: the rotations of a round act on disjoint index
+        // pairs, so J^T A J splits into independent 2x2 blocks
+        // B'(k1,k2) = J_k1^T B(k1,k2) J_k2 (upper blocks, mirrored), and Q <- Q J
+        // row by row; only the live n x n part is touched.
+        for (int e = threadIdx.x; e < npairs * npairs + npairs * n; e += blockDim.x) {
+          if (e < npairs * npairs) {
+            const int k1 = e / npairs, k2 = e - k1 * npairs;
+            if (k1 > k2) continue;
+            const double s1 = cs_s[k1], s2 = cs_s[k2];
+            if (s1 == 0.0 && s2 == 0.0) continue;
+            const double c1 = cs_c[k1], c2 = cs_c[k2];
+            const int p1 = pp[k1], q1 = pq[k1], p2 = pp[k2], q2 = pq[k2];
+            const double a = A[p1 + ld * p2], b = A[p1 + ld * q2];
+            const double c = A[q1 + ld * p2], d = A[q1 + ld * q2];
+            // columns (B J2), then rows (J1^T .)
+            const double ap = c2 * a - s2 * b, bq = s2 * a + c2 * b;
+            const double cp = c2 * c - s2 * d, dq = s2 * c + c2 * d;
+            const double npp = c1 * ap - s1 * cp, npq = c1 * bq - s1 * dq;
+            const double nqp = s1 * ap + c1 * cp, nqq = s1 * bq + c1 * dq;
+            A[p1 + ld * p2] = npp;
+            A[p1 + ld * q2] = npq;
+            A[q1 + ld * p2] = nqp;
+            A[q1 + ld * q2] = nqq;
+            if (k1 != k2) {
+              A[p2 + ld * p1] = npp;
+              A[q2 + ld * p1] = npq;
+              A[p2 + ld * q1] = nqp;
+              A[q2 + ld * q1] = nqq;
+            }
+          } else {
+            const int e2 = e - npairs * npairs;
+            const int k = e2 / n, i = e2 - k * n;
+            const double sn = cs_s[k];
+            if (sn == 0.0) continue;
+            const double c = cs_c[k];
+            const int p = pp[k], q = pq[k];
+            const double qp = Q[i + ld * p], qq = Q[i + ld * q];
+            Q[i + ld * p] = c * qp - sn * qq;
+            Q[i + ld * q] = sn * qp + c * qq;
+          }
+        }
+        __syncthreads();
+      }
+      // converged once a whole sweep needed no rotation (every |a_pq| is below
+      // 1e-15 sqrt(|a_pp a_qq|), the classical Jacobi stopping rule)
+      const int any = rot_any;
+      __syncthreads();
+      if (threadIdx.x == 0) rot_any = 0;
+      __syncthreads();
+      if (threadIdx.x == 0) atomicAdd(&g_dbg[0], 1);  // ritz sweeps
+      if (!any) break;
+    }
   }
   // descending order (stable on ties, like reversing eigh's ascending output)
   if (threadIdx.x == 0) {
