@@ -229,8 +229,14 @@ def admm_bytes(shape, esize, nmodes=3):
     fft = (T + S) + (d - 2) * 2 * S + 2 * S + (d - 2) * 2 * S + (S + T)
     return {
         "fft": fft,
+        # first sweep of a solve only (later sweeps get rhs from the fused tail)
         "admm_rhs": (3 + 2 * nmodes) * T + T,
-        "lrta_input": nmodes * 3 * T,
+        # L once + nmodes multipliers in, nmodes LRTA inputs out
+        "lrta_input": (1 + 2 * nmodes) * T,
+        # fused tail: L, L_prev, A, E, Y, mask + (G_new, G_old, lag) per mode in;
+        # lag' per mode, E', Y', next rhs out
+        "sweep_tail": (5 + 3 * nmodes) * T + N + (3 + nmodes) * T,
+        # unfused fallbacks
         "lag_update": nmodes * 5 * T,
         "noise_dual": 6 * T + 2 * T + N,
     }

@@ -106,6 +106,16 @@ static int64_t grid_for(int64_t n) {
   return std::max<int64_t>(1, std::min<int64_t>(cdiv(n, kRedThreads), (int64_t)num_sms() * 8));
 }
 
+// Resident grid of a line kernel (SMs x occupancy, capped by grid_for): all
+// blocks run concurrently, which the stencil kernels rely on for L2 reuse.
+template <typename K>
+static unsigned resident_grid(K kernel, int64_t n) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kRedThreads, 0);
+  const int64_t cap = grid_for<float>(n);
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(cap, (int64_t)std::max(per_sm, 1) * num_sms()));
+}
+
 // forward FFT over all axes, diagonal solve in the last-axis pass, inverse FFT
 // Spectrum geometry: half spectrum along axis 0 (n0/2+1 bins) when n0 is even
 // (real-to-complex first pass), the full complex spectrum otherwise.
@@ -441,8 +451,8 @@ static void lrta_inputs(Solver<T>& s, const T* x, double mu, bool v4, unsigned g
       xs.p[k] = s.X[k0 + k];
       lg.axis[k] = xs.axis[k] = s.cfg.modes[k0 + k];
     }
-    launch("lrta_input", v4 ? k_lrta_input<T, 4> : k_lrta_input<T, 1>, grid, kRedThreads, 0, st,
-           s.g, x, lg, xs, mu);
+    const auto kern = v4 ? k_lrta_input<T, 4> : k_lrta_input<T, 1>;
+    launch("lrta_input", kern, resident_grid(kern, s.g.N), kRedThreads, 0, st, s.g, x, lg, xs, mu);
   }
 }
 
@@ -522,8 +532,10 @@ static int admm_step(Solver<T>& s, double* hout) {
         gn.axis[k] = go.axis[k] = lw.axis[k] = s.cfg.modes[k];
       }
       const double mu_next = std::min(s.cfg.mu_max, s.cfg.growth * mu);
+      unsigned tgrid = 0;
 #define TR_ST2(K, S)                                                                            \
-  launch("sweep_tail", k_sweep_tail<T, K, S>, grid, kRedThreads, 0, st, g, s.A, s.mask,         \
+  tgrid = resident_grid(k_sweep_tail<T, K, S>, N);                                              \
+  launch("sweep_tail", k_sweep_tail<T, K, S>, tgrid, kRedThreads, 0, st, g, s.A, s.mask,        \
          (const T*)s.l, (const T*)s.lold, s.e, s.y, gn, go, lp, lw, mu, mu_next, q0, q1, level, \
          (const double*)s.scale, s.rhs, part)
 #define TR_ST(K)                 \
@@ -537,7 +549,7 @@ static int admm_step(Solver<T>& s, double* hout) {
 #undef TR_ST
 #undef TR_ST2
       // partial slots: 5 per mode (4 slots) then the 7 noise values -> res[96..122]
-      launch("final_reduce", k_final_reduce, 1, 256, 0, st, (const double*)part, (int)rb, 27,
+      launch("final_reduce", k_final_reduce, 1, 256, 0, st, (const double*)part, (int)tgrid, 27,
              0b0010101u << 20 | 0b00101u | 0b00101u << 5 | 0b00101u << 10 | 0b00101u << 15,
              res + 96);
       for (int k = 0; k < nm; ++k) std::swap(s.lag[k], s.lag2[k]);

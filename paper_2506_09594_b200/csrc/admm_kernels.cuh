@@ -124,31 +124,21 @@ struct LineCo {
   int co[kMaxOrder];
 };
 
-// Walk every V-element chunk of every axis-0 line: f(lc, i0).  Long lines are
-// split across the block's threads, and each block takes a contiguous range of
-// an enumeration of the lines in which the LAST axis runs fastest: a line's
-// neighbours along the outer axes are then this block's previous / next lines
-// or lines that adjacent blocks touch at the same time, so the stencil
-// re-reads hit L2.  Short lines pack several per pass.
+// Walk every V-element chunk of every axis-0 line: f(lc, i0).  Long lines:
+// grid-stride over the lines in memory order with a RESIDENT grid (the host
+// sizes it to SMs x occupancy), so every block advances in lockstep and a
+// line's neighbours along the outer axes (+-1 line, +-n1 lines, ...) are read
+// by some block within about one iteration -- the stencil re-reads hit L2.
+// Short lines pack several per pass.
 template <int V, typename F>
 __device__ __forceinline__ void for_each_chunk(const Geom& g, F&& f) {
   const int64_t n0 = g.dims[0], lines = g.N / n0;
   const int cpl = (int)(n0 / V);
   LineCo lc;
   if (cpl >= (int)blockDim.x) {
-    const int64_t per = (lines + gridDim.x - 1) / gridDim.x;
-    const int64_t j0 = (int64_t)blockIdx.x * per, j1 = min(lines, j0 + per);
-    for (int64_t j = j0; j < j1; ++j) {
-      int64_t r = j, line = 0;
-      for (int a = g.d - 1; a >= 1; --a) {
-        const int64_t n = g.dims[a];
-        const int64_t q = (r < (1ll << 31) && n < (1ll << 31))
-                              ? (int64_t)((uint32_t)r / (uint32_t)n) : r / n;
-        lc.co[a] = (int)(r - q * n);
-        line += (r - q * n) * g.lst[a];
-        r = q;
-      }
+    for (int64_t line = blockIdx.x; line < lines; line += gridDim.x) {
       lc.line = line;
+      for (int a = 1; a < g.d; ++a) lc.co[a] = (int)line_coord(g, line, a);
       for (int c = threadIdx.x; c < cpl; c += blockDim.x) f(lc, (int64_t)c * V);
     }
   } else {
