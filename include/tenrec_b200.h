@@ -81,6 +81,27 @@ int tr_gnhtsvt_randomized(int dtype, const void* a, void* out, int order, const 
                           int64_t workspace_bytes, void* stream);
 
 /*
+ * Sharded randomized t-SVT (multi-GPU, one rank per GPU): this rank holds the
+ * slice [last_off, last_off + dims[order-1]) of the LAST mode of a tensor whose
+ * last mode has length last_all (`dims` are the LOCAL dims; earlier modes
+ * whole).  The mode-0/1 Krylov partial sums, the Ritz Gram and the compressed
+ * r0 x r1 x faces core are summed across ranks through `allreduce` (in place,
+ * fp64, ordered on `stream`; e.g. NCCL through torch.distributed), the sketch
+ * is drawn at GLOBAL column indices, so every rank's `out` slice equals the
+ * same slice of the single-GPU tr_gnhtsvt_randomized result up to summation
+ * order.  Workspace: tr_lrta_workspace of the GLOBAL dims.  Returns 0 / error.
+ */
+typedef int (*tr_allreduce_fn)(double* buf, int64_t count, void* stream, void* user);
+int tr_gnhtsvt_randomized_sharded(int dtype, const void* a, void* out, int order,
+                                  const int64_t* dims, int64_t last_all, int64_t last_off,
+                                  const int64_t* ranks, const int64_t* blocks,
+                                  const int64_t* krylov, uint64_t seed, int transform_kind,
+                                  const void* transform_mats, const double* alphas,
+                                  int penalty_kind, double p0, double p1, double tau,
+                                  tr_allreduce_fn allreduce, void* user, void* workspace,
+                                  int64_t workspace_bytes, void* stream);
+
+/*
  * Fixed-rank Tucker compression of modes (0, 1) -- replaces
  * tenrec.sketch.rsthosvd_bki(x, ranks, order=(0, 1), ...) (sketch.py:211-270).
  * Outputs (device, fp64, zero-padded to the requested ranks):

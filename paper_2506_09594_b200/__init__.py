@@ -12,6 +12,7 @@ from .penalties import (PENALTY_NAMES, L1, MCP, SCAD, CappedLq, Firm, LogPenalty
 from .gradient import GradientSet, solve_grad_system
 from .onebit import (ObservationSet, data_fit_update, gnobhtc, gnobrhtc, naive_estimate,
                      onebit_observe)
+from .shard import DeviceAllreduce, gnhtsvt_randomized_sharded, shard_range
 from .sketch import SketchConfig, TuckerFactors, gnhtsvt_randomized, rsthosvd_bki
 from .solvers import SolveReport, SolverConfig, default_lambda, gnhtc, gnrhtc
 from .transform import DEFAULT_TRANSFORM, Transform, TransformError
@@ -23,5 +24,5 @@ __all__ = [
     "make_penalty", "SketchConfig", "TuckerFactors", "gnhtsvt_randomized", "rsthosvd_bki",
     "DEFAULT_TRANSFORM", "Transform", "TransformError", "SolveReport", "SolverConfig",
     "default_lambda", "gnhtc", "gnrhtc", "ObservationSet", "data_fit_update", "gnobhtc",
-    "gnobrhtc", "naive_estimate", "onebit_observe", "GradientSet", "solve_grad_system",
+    "gnobrhtc", "naive_estimate", "onebit_observe", "GradientSet", "solve_grad_system", "DeviceAllreduce", "gnhtsvt_randomized_sharded", "shard_range",
 ]

@@ -20,6 +20,10 @@ _c_i64p = ctypes.POINTER(ctypes.c_int64)
 _c_dp = ctypes.POINTER(ctypes.c_double)
 _vp = ctypes.c_void_p
 
+# int (*tr_allreduce_fn)(double* buf, int64_t count, void* stream, void* user)
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_int64,
+                                ctypes.c_void_p, ctypes.c_void_p)
+
 # name -> (restype, argtypes); the list is the contract tests check against the header
 SIGNATURES = {
     "tr_version": (ctypes.c_int, []),
@@ -30,6 +34,11 @@ SIGNATURES = {
         ctypes.c_int, _vp, _vp, ctypes.c_int, _c_i64p, _c_i64p, _c_i64p, _c_i64p, ctypes.c_uint64,
         ctypes.c_int, _vp, _c_dp, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double,
         _vp, _vp, _vp, ctypes.c_int64, _vp]),
+    "tr_gnhtsvt_randomized_sharded": (ctypes.c_int, [
+        ctypes.c_int, _vp, _vp, ctypes.c_int, _c_i64p, ctypes.c_int64, ctypes.c_int64, _c_i64p,
+        _c_i64p, _c_i64p, ctypes.c_uint64, ctypes.c_int, _vp, _c_dp, ctypes.c_int,
+        ctypes.c_double, ctypes.c_double, ctypes.c_double, ALLREDUCE_FN, _vp, _vp,
+        ctypes.c_int64, _vp]),
     "tr_rsthosvd_bki": (ctypes.c_int, [
         ctypes.c_int, _vp, ctypes.c_int, _c_i64p, _c_i64p, _c_i64p, _c_i64p, ctypes.c_uint64,
         _vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int64, _vp]),

@@ -45,12 +45,27 @@ struct Carve {
   }
 };
 
+// In-place fp64 sum across the ranks of a sharded t-SVT, ordered on `stream`
+// (tenrec_b200.h: tr_allreduce_fn).  Null = one rank.
+typedef int (*AllreduceFn)(double* buf, int64_t count, void* stream, void* user);
+
 struct Shape {
   int order;
-  int64_t n1, n2, nf;
-  Trailing tr;
+  int64_t n1, n2, nf;  // nf: this rank's faces (trailing modes flattened)
+  Trailing tr;         // GLOBAL trailing dims (the transform runs on the whole core)
   int64_t r0, r1, b0, b1, q0, q1, s0, s1;
+  int64_t nf_all = 0, f0 = 0;  // all faces, index of this rank's first face
+  AllreduceFn coll = nullptr;
+  void* coll_user = nullptr;
+  int64_t faces_all() const { return nf_all > 0 ? nf_all : nf; }
 };
+
+static int allreduce(const Shape& sh, double* buf, int64_t count, cudaStream_t st) {
+  if (!sh.coll) return 0;
+  TR_LAUNCH_CHECK();
+  TR_REQUIRE(sh.coll(buf, count, (void*)st, sh.coll_user) == 0, "all-reduce callback failed");
+  return 0;
+}
 
 static int make_shape(int order, const int64_t* dims, const int64_t* ranks, const int64_t* blocks,
                       const int64_t* krylov, Shape& sh) {
@@ -135,9 +150,9 @@ static void carve(Carve& cv, const Shape& sh, Bufs<T>& b) {
   b.F1t = cv.take<T>(sh.n2 * sh.r1);
   b.A1 = cv.take<T>(sh.n2 * nA1);
   b.C1 = cv.take<T>(sh.r0 * sh.n2 * sh.nf);
-  b.core = cv.take<double>(sh.r0 * sh.r1 * sh.nf);
-  b.cf0 = cv.take<cplx>(sh.r0 * sh.r1 * sh.nf);
-  b.cf1 = cv.take<cplx>(sh.r0 * sh.r1 * sh.nf);
+  b.core = cv.take<double>(sh.r0 * sh.r1 * sh.faces_all());
+  b.cf0 = cv.take<cplx>(sh.r0 * sh.r1 * sh.faces_all());
+  b.cf1 = cv.take<cplx>(sh.r0 * sh.r1 * sh.faces_all());
   int64_t usz = 0;
   for (int i = 0; i < sh.tr.nt; ++i) usz += sh.tr.d[i] * sh.tr.d[i];
   b.U = cv.take<cplx>(usz);
@@ -348,14 +363,15 @@ static bool project(const double*, int64_t, int64_t, int, Bufs<double>&, cudaStr
 // Leaves the factor in F (fp64) / Ft, the eigenvectors V (s x r) and
 // W = A^T Z (n x s) for the core; info[0] = s_eff, info[1] = r_eff.
 template <typename T>
-static int bki_mode(const T* A, int64_t m, int64_t n, int r, int b, int q, SketchSpec sk,
-                    const T* gover, Bufs<T>& bf, double* V, double* F, T* Ft, int64_t* info,
-                    cudaStream_t st) {
+static int bki_mode(const Shape& sh, const T* A, int64_t m, int64_t n, int r, int b, int q,
+                    SketchSpec sk, const T* gover, Bufs<T>& bf, double* V, double* F, T* Ft,
+                    int64_t* info, cudaStream_t st) {
   const int s = (q + 1) * b;
   const bool fused = panel_ok<T>(A, m, b);
   int64_t np = fused ? panel<T, 0>(A, m, n, b, nullptr, gover, sk, bf.partial, st)
                      : rank_update<T>(A, m, n, b, nullptr, gover, sk, bf.partial, st);
   reduce(bf.partial, np, m * b, bf.K, st);
+  if (allreduce(sh, bf.K, m * b, st)) return 1;  // columns are sharded: sum the ranks
   launch("normalize_piece", k_normalize_piece<T>, 1, 1024, 0, st, bf.K, m * b, bf.P);
   for (int k = 1; k <= q; ++k) {
     if (fused) {
@@ -366,6 +382,7 @@ static int bki_mode(const T* A, int64_t m, int64_t n, int r, int b, int q, Sketc
     }
     double* slot = bf.K + m * (int64_t)b * k;
     reduce(bf.partial, np, m * b, slot, st);
+    if (allreduce(sh, slot, m * b, st)) return 1;
     launch("normalize_piece", k_normalize_piece<T>, 1, 1024, 0, st, slot, m * b, bf.P);
   }
   orth_basis<T>(m, s, bf, info, st);
@@ -381,6 +398,7 @@ static int bki_mode(const T* A, int64_t m, int64_t n, int r, int b, int q, Sketc
              bf.Mpart);
     reduce(bf.Mpart, mp, (int64_t)s * s, bf.M, st);
   }
+  if (allreduce(sh, bf.M, (int64_t)s * s, st)) return 1;  // W rows are sharded
   if (s <= kJW && g_use_warp_jacobi) {
     const size_t sm = 4 * kJW * kVld * sizeof(double);
     static bool attr = false;
@@ -408,20 +426,25 @@ static int lrta_compress(const T* a, const Shape& sh, uint64_t seed, const T* g0
   }
   const int64_t nA0 = sh.n2 * sh.nf, nA1 = sh.r0 * sh.nf;
   // mode 0 on the tensor itself (m = n1, n = n2 * nf)
-  SketchSpec sk0{seed, 0, nA0, nullptr};
-  if (bki_mode<T>(a, sh.n1, nA0, (int)sh.r0, (int)sh.b0, (int)sh.q0, sk0, g0, bf, bf.V0, bf.F0,
-                  bf.F0t, bf.info, st))
+  SketchSpec sk0{seed, 0, sh.n2 * sh.faces_all(), nullptr, sh.n2 * sh.f0};
+  if (bki_mode<T>(sh, a, sh.n1, nA0, (int)sh.r0, (int)sh.b0, (int)sh.q0, sk0, g0, bf, bf.V0,
+                  bf.F0, bf.F0t, bf.info, st))
     return 2;
   // core rows -> mode-1 unfolding (n2 x r0*nf), contiguous columns
   launch("core_from_w", k_core_from_w<T, T>, (unsigned)cdiv(nA0, 256), 256, 0, st,
       bf.W, nA0, (int)sh.s0, bf.V0, (int)sh.r0, sh.n2, bf.A1);
   // mode 1 on the core (m = n2, n = r0 * nf); logical columns use r0_eff
-  SketchSpec sk1{seed, 1, sh.r0, bf.info + 1};
-  if (bki_mode<T>(bf.A1, sh.n2, nA1, (int)sh.r1, (int)sh.b1, (int)sh.q1, sk1, g1, bf, bf.V1,
+  SketchSpec sk1{seed, 1, sh.r0, bf.info + 1, sh.r0 * sh.f0};
+  if (bki_mode<T>(sh, bf.A1, sh.n2, nA1, (int)sh.r1, (int)sh.b1, (int)sh.q1, sk1, g1, bf, bf.V1,
                   bf.F1, bf.F1t, bf.info + 2, st))
     return 2;
+  // this rank's faces of the r0 x r1 x faces core; sharded: zero the rest and
+  // sum the ranks, so every rank holds the whole core for the transform-domain SVT
+  const int64_t face = sh.r0 * sh.r1;
+  if (sh.coll) TR_CUDA(cudaMemsetAsync(bf.core, 0, sizeof(double) * face * sh.faces_all(), st));
   launch("core_from_w", k_core_from_w<T, double>, (unsigned)cdiv(nA1, 256), 256, 0, st,
-      bf.W, nA1, (int)sh.s1, bf.V1, (int)sh.r1, sh.r0, bf.core);
+      bf.W, nA1, (int)sh.s1, bf.V1, (int)sh.r1, sh.r0, bf.core + face * sh.f0);
+  if (allreduce(sh, bf.core, face * sh.faces_all(), st)) return 2;
   TR_LAUNCH_CHECK();
   return 0;
 }
@@ -447,7 +470,8 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
     }
     uoff += (int64_t)n * n;
   }
-  const int64_t total = face * sh.nf;
+  const int64_t nfa = sh.faces_all();
+  const int64_t total = face * nfa;
   const unsigned g = (unsigned)cdiv(total, 256);
   // forward: mode products along trailing modes 2..d-1
   const void* src = bf.core;
@@ -457,7 +481,7 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
   int64_t st_lo = face;
   for (int i = 0; i < nt; ++i) {
     const int n = (int)sh.tr.d[i];
-    const int64_t hi = sh.nf / (st_lo / face) / n;
+    const int64_t hi = nfa / (st_lo / face) / n;
     launch("mode_product", k_mode_product, g, 256, 0, st, src, src_real, bufs[cur], 0, st_lo, n, hi, U[i], 0, 1.0);
     src = bufs[cur];
     src_real = 0;
@@ -480,18 +504,18 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
                                    (int)sm));
       wattr = true;
     }
-    launch("face_svt", k_face_svt_warp, (unsigned)cdiv(sh.nf, 4), 128, sm, st, (double2*)faces,
-           (int)sh.r0, (int)sh.r1, sh.nf, pen, tau);
+    launch("face_svt", k_face_svt_warp, (unsigned)cdiv(nfa, 4), 128, sm, st, (double2*)faces,
+           (int)sh.r0, (int)sh.r1, nfa, pen, tau);
   } else {
-    launch("face_svt", k_face_svt, (unsigned)sh.nf, 1024, smem, st, faces, (int)sh.r0,
+    launch("face_svt", k_face_svt, (unsigned)nfa, 1024, smem, st, faces, (int)sh.r0,
            (int)sh.r1, pen, tau);
   }
-  if (kind == TR_TRANSFORM_FFT) launch("mirror_fix", k_mirror_fix, g, 256, 0, st, faces, face, sh.nf, sh.tr);
+  if (kind == TR_TRANSFORM_FFT) launch("mirror_fix", k_mirror_fix, g, 256, 0, st, faces, face, nfa, sh.tr);
   // inverse: U^H / alpha in reverse mode order, real part on the last step
   for (int i = nt - 1; i >= 0; --i) {
     const int n = (int)sh.tr.d[i];
     st_lo /= n;
-    const int64_t hi = sh.nf / (st_lo / face) / n;
+    const int64_t hi = nfa / (st_lo / face) / n;
     const bool last = (i == 0);
     void* dst = last ? (void*)bf.core : (void*)bufs[cur];
     launch("mode_product", k_mode_product, g, 256, 0, st, src, 0, dst, last ? 1 : 0, st_lo, n, hi, U[i], 1, al[i]);
@@ -505,8 +529,9 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
 template <typename T>
 static int expand(const Shape& sh, Bufs<T>& bf, T* out, cudaStream_t st) {
   const int64_t N = sh.n2 * sh.nf;
-  launch("expand_mode1", k_expand_mode1<T>, (unsigned)cdiv(sh.r0 * N, 256), 256, 0, st, 
-      bf.core, (int)sh.r0, (int)sh.r1, sh.nf, bf.F1, sh.n2, bf.C1);
+  launch("expand_mode1", k_expand_mode1<T>, (unsigned)cdiv(sh.r0 * N, 256), 256, 0, st,
+         (const double*)(bf.core + sh.r0 * sh.r1 * sh.f0), (int)sh.r0, (int)sh.r1, sh.nf, bf.F1,
+         sh.n2, bf.C1);
   constexpr int RA = 8, CB = sizeof(T) == 4 ? 16 : 8;
   const int64_t nrb = cdiv(sh.n1, 32 * RA);
   const int64_t kp = cdiv(sh.r0, 16 / (int64_t)sizeof(T)) * (16 / (int64_t)sizeof(T));
@@ -623,6 +648,44 @@ int tr_gnhtsvt_randomized(int dtype, const void* a, void* out, int order, const 
   TR_REQUIRE(dtype == TR_F64, "bad dtype %d", dtype);
   return gnhtsvt_randomized_t<double>(a, out, sh, seed, transform_kind, transform_mats, alphas,
                                       pen, tau, sketch0, sketch1, workspace, workspace_bytes, st);
+}
+
+int tr_gnhtsvt_randomized_sharded(int dtype, const void* a, void* out, int order,
+                                  const int64_t* dims, int64_t last_all, int64_t last_off,
+                                  const int64_t* ranks, const int64_t* blocks,
+                                  const int64_t* krylov, uint64_t seed, int transform_kind,
+                                  const void* transform_mats, const double* alphas,
+                                  int penalty_kind, double p0, double p1, double tau,
+                                  tr_allreduce_fn allreduce, void* user, void* workspace,
+                                  int64_t workspace_bytes, void* stream) {
+  Shape sh;
+  if (make_shape(order, dims, ranks, blocks, krylov, sh)) return 1;
+  const int64_t last = dims[order - 1];
+  TR_REQUIRE(last_all >= 1 && last_off >= 0 && last_off + last <= last_all,
+             "shard [%lld, %lld) outside the last mode of length %lld", (long long)last_off,
+             (long long)(last_off + last), (long long)last_all);
+  TR_REQUIRE(transform_kind >= 0 && transform_kind <= 2, "bad transform kind %d", transform_kind);
+  TR_REQUIRE(transform_kind != TR_TRANSFORM_EXPLICIT || (transform_mats && alphas),
+             "explicit transform needs matrices and alphas");
+  TR_REQUIRE(penalty_kind >= 0 && penalty_kind <= 6, "bad penalty kind %d", penalty_kind);
+  TR_REQUIRE(tau >= 0.0, "tau must be >= 0");
+  TR_REQUIRE(a && out && workspace, "null pointer argument");
+  // faces = trailing modes flattened (last mode slowest): this rank owns a
+  // contiguous block of them; the transform sees the global trailing dims
+  const int64_t inner = sh.nf / last;
+  sh.tr.d[order - 3] = last_all;
+  sh.nf_all = inner * last_all;
+  sh.f0 = inner * last_off;
+  sh.coll = allreduce;
+  sh.coll_user = user;
+  Penalty pen{penalty_kind, p0, p1};
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == TR_F32)
+    return gnhtsvt_randomized_t<float>(a, out, sh, seed, transform_kind, transform_mats, alphas,
+                                       pen, tau, nullptr, nullptr, workspace, workspace_bytes, st);
+  TR_REQUIRE(dtype == TR_F64, "bad dtype %d", dtype);
+  return gnhtsvt_randomized_t<double>(a, out, sh, seed, transform_kind, transform_mats, alphas,
+                                      pen, tau, nullptr, nullptr, workspace, workspace_bytes, st);
 }
 
 int tr_rsthosvd_bki(int dtype, const void* a, int order, const int64_t* dims,

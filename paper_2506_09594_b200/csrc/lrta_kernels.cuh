@@ -20,6 +20,7 @@ struct SketchSpec {
   uint64_t stream;
   int64_t inner;
   const int64_t* inner_eff;  // device scalar or nullptr
+  int64_t col0 = 0;          // global index of local column 0 (sharded unfoldings)
 };
 
 // partial[p][j][i] = sum_{c in split p} A[i + m c] * C(c, j)
@@ -49,7 +50,7 @@ __global__ void __launch_bounds__(256) k_rank_update(
         if (coef) {
           v = coef[c * b + j];
         } else {
-          const int64_t lo = c % sk.inner, f = c / sk.inner;
+          const int64_t lo = (c + sk.col0) % sk.inner, f = (c + sk.col0) / sk.inner;
           if (lo < eff) {
             const int64_t cl = lo + eff * f;
             v = gover ? gover[cl * b + j] : (T)gauss_at(sk.seed, sk.stream, (uint64_t)(cl * b + j));

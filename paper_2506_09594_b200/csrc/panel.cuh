@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
         const int c = e / B, j = e % B;
         T v = T(0);
         if (c < cols && j < pa.b) {
-          const int64_t col = c0 + c;
+          const int64_t col = c0 + c + pa.sk.col0;  // global column
           const int64_t lo = col % pa.sk.inner, f = col / pa.sk.inner;
           if (lo < eff) {
             const int64_t cl = lo + eff * f;

@@ -128,11 +128,14 @@ _WORKSPACES = {}
 
 
 def workspace(nbytes: int):
-    """Cached device workspace of at least ``nbytes`` (per device)."""
+    """Cached device workspace of at least ``nbytes`` (per device and host thread:
+    concurrent host threads never share one)."""
+    import threading
+
     torch = _torch()
-    dev = torch.cuda.current_device()
-    buf = _WORKSPACES.get(dev)
+    key = (torch.cuda.current_device(), threading.get_ident())
+    buf = _WORKSPACES.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device="cuda")
-        _WORKSPACES[dev] = buf
+        _WORKSPACES[key] = buf
     return buf
