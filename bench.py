@@ -2,7 +2,7 @@
 """Benchmark of the B200 randomized t-SVT / ADMM hot path ("Measurement").
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--step admm|lrta]
+                    [--step admm|lrta|tsvt-sharded]
 
 Workload (BASELINE.json configs[1]): order-3 robust tensor PCA, 1024x1024x128
 float32, tubal rank 20 from Gaussian factors (unit RMS), 10% sparse outliers
@@ -14,7 +14,10 @@ A step (``--step admm``, default) is one ADMM sweep of tenrec.solvers.gnrhtc:
 FFT-diagonal L-solve, three randomized t-SVTs (one per gradient mode), noise /
 dual / multiplier updates, Eq. (24) residuals back to the host.  Metric:
 randomized t-SVT voxels/s = 3 x 1024*1024*128 x sweeps/s (whole job); ADMM
-sweeps/s is reported beside it.  ``--step lrta`` times a single t-SVT.  Every
+sweeps/s is reported beside it.  ``--step lrta`` times a single t-SVT;
+``--step tsvt-sharded`` times one t-SVT of the whole tensor sharded along its
+last mode over the N ranks (strong scaling, NCCL all-reduces of the Krylov
+blocks / Ritz Gram / core, shard.py).  Every
 tensor is 512 MB (> 126 MB L2), so no explicit flush is needed.
 
 Multi-GPU: one process per GPU (torchrun); each rank solves its own problem
@@ -273,12 +276,22 @@ def run_ours(args):
     rank = _env_int("RANK", 0)
     local = _env_int("LOCAL_RANK", 0)
     torch.cuda.set_device(local)
+    sharded = args.step == "tsvt-sharded"
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif sharded:  # a one-rank NCCL group for the same code path
+        import socket
+
+        with socket.socket() as sock:
+            sock.bind(("127.0.0.1", 0))
+            port = sock.getsockname()[1]
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                                world_size=1, device_id=torch.device("cuda", local))
     lib = _lib.lib()
     dims = WORKLOAD["dims"]
     N = math.prod(dims)
-    flat = make_workload(torch, dims, 1234 + rank)
+    # replicas: a problem per rank; sharded: the same tensor on every rank
+    flat = make_workload(torch, dims, 1234 if sharded else 1234 + rank)
     cm = ColMajor(flat, dims, "torch", None)
     sk = pk.SketchConfig(mode="fixed-rank", order=(0, 1), ranks=WORKLOAD["ranks"],
                          blocks=WORKLOAD["blocks"], krylov=WORKLOAD["krylov"], seed=7)
@@ -294,6 +307,19 @@ def run_ours(args):
 
         def step():
             run.step()
+    elif sharded:
+        off, cnt = pk.shard_range(dims[-1], world, rank)
+        face = dims[0] * dims[1]
+        ldims = (dims[0], dims[1], cnt)
+        cm_l = ColMajor(flat[face * off:face * (off + cnt)], ldims, "torch", None)
+        tau = 0.05 * float(flat.norm()) / math.sqrt(N)
+        stream = torch.cuda.current_stream()
+        lrta_per_step = 1.0 / world  # every rank's step is 1/world of one t-SVT
+        red = pk.DeviceAllreduce()
+
+        def step():
+            pk.gnhtsvt_randomized_sharded(cm_l, dims[-1], off, pk.Transform.fft(), pk.MCP(2.5),
+                                          tau, sk, allreduce=red)
     else:
         out = ColMajor(torch.empty_like(flat), dims, "torch", None)
         tau = 0.05 * float(flat.norm()) / math.sqrt(N)
@@ -338,7 +364,27 @@ def run_ours(args):
     host = flat.reshape(tuple(reversed(dims))).permute(2, 1, 0).cpu().numpy()
     host_mask = np.ones(dims, dtype=bool)
     e2e_iters = max(10, args.steps)
-    if args.step == "admm":
+    if sharded:
+        tf = pk.Transform.fft()
+        host_l = np.ascontiguousarray(host[..., off:off + cnt])
+        pk.gnhtsvt_randomized_sharded(host_l, dims[-1], off, tf, pk.MCP(2.5), tau, sk,
+                                      allreduce=red)
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_iters):
+            res = pk.gnhtsvt_randomized_sharded(host_l, dims[-1], off, tf, pk.MCP(2.5), tau, sk,
+                                                allreduce=red)
+        e2e_s = (time.perf_counter() - t0) / e2e_iters
+        if world > 1:
+            t = torch.tensor([e2e_s], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": N / e2e_s, "unit": UNIT, "h2d_bytes_per_step": host_l.nbytes,
+               "d2h_bytes_per_step": res.nbytes,
+               "api": "paper_2506_09594_b200.gnhtsvt_randomized_sharded(numpy slice)",
+               "per_rank_bytes": True}
+    elif args.step == "admm":
         cfg_e2e = pk.SolverConfig(phi=pk.MCP(2.5), psi=pk.MCP(2.5), randomized=True, sketch=sk,
                                   max_iters=e2e_iters, tol=1e-30)
         # untimed warm-up call: page-locked staging blocks and the solver's
@@ -397,12 +443,14 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+            "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded Gaussian-factor t-product + uniform outliers)",
             "config": {"workload": WORKLOAD["workload"], "step": args.step, "dims": list(dims),
                        "ranks": list(WORKLOAD["ranks"]), "blocks": list(WORKLOAD["blocks"]),
                        "krylov": list(WORKLOAD["krylov"]), "gradient_modes": list(WORKLOAD["modes"]),
-                       "parallelism": f"replicas{world}",
+                       "parallelism": (f"last-mode-shard{world}" if sharded
+                                       else f"replicas{world}"),
                        "l2": "every tensor 512 MB > 126 MB L2 (no flush needed)"},
             "admm_iters_per_s": (1e3 / ms_per_step) if args.step == "admm" else None,
             "e2e": e2e, "gpu_launches": launches, "roofline": roof,
@@ -411,7 +459,7 @@ def run_ours(args):
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args.step)
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 or sharded:
         dist.destroy_process_group()
 
 
@@ -507,7 +555,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--step", choices=("admm", "lrta"), default="admm")
+    ap.add_argument("--step", choices=("admm", "lrta", "tsvt-sharded"), default="admm")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
