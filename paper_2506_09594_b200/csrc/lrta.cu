@@ -13,6 +13,7 @@
 #include "tsqr.cuh"
 #include "jacobi.cuh"
 #include "panel.cuh"
+#include "panel_mma.cuh"
 #include "proj_tc.cuh"
 #include "prof.cuh"
 
@@ -149,7 +150,7 @@ static void carve(Carve& cv, const Shape& sh, Bufs<T>& b) {
   b.M = cv.take<double>(smax * smax);
   b.Zt = cv.take<T>(mmax * smax);
   b.P = cv.take<T>(mmax * bmax);
-  b.coef = cv.take<T>(nmax * bmax);
+  b.coef = cv.take<T>((nmax + 16) * bmax);  // + chunk pad of the sketch rows
   b.W = cv.take<T>(nmax * smax);
   b.V0 = cv.take<double>(sh.s0 * sh.r0);
   b.V1 = cv.take<double>(sh.s1 * sh.r1);
@@ -233,9 +234,65 @@ static int64_t panel_launch(const T* A, const T* P, const T* gover, PanelArgs pa
   return grid;
 }
 
+// Tensor-core Krylov pass (panel_mma.cuh): fp32 unfoldings with m <= 1024, b <= 8.
+template <int RG, int MODE>
+static int64_t panel_mma_launch(const float* A, const float* P, const float* coef,
+                                PanelMmaArgs pa, double* partial, cudaStream_t st) {
+  const size_t fixed =
+      MODE ? (size_t)(2 * kPmWarps * kPmRS + 4 * kPmTE) * sizeof(float) : 0;
+  const size_t stage =
+      (size_t)kPmCols * pa.S * sizeof(float) + (MODE ? 0 : (size_t)kPmCols * pa.b * sizeof(float));
+  pa.nst = (int)std::min<size_t>(kPmMaxStages, (220 * 1024 - fixed) / stage);
+  static const int nst_cap = getenv("TR_PM_STAGES") ? atoi(getenv("TR_PM_STAGES")) : 0;
+  if (nst_cap >= 2) pa.nst = std::min(pa.nst, nst_cap);
+  const int64_t grid = std::min<int64_t>(pa.nchunks, stream_sms());
+  const size_t smem = pa.nst * stage + fixed;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_panel_mma<RG, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         220 * 1024);
+    attr = true;
+  }
+  launch(MODE ? "panel_gram" : "panel_sketch", k_panel_mma<RG, MODE>, (unsigned)grid, kPmThreads,
+         smem, st, A, P, coef, pa, partial);
+  return grid;
+}
+
+// MODE 0 draws the sketch rows into `rows` ((n + 16) x b scratch) first.
+template <int MODE>
+static int64_t panel_mma(const float* A, int64_t m, int64_t n, int b, const float* P,
+                         const float* gover, SketchSpec sk, float* rows, double* partial,
+                         cudaStream_t st) {
+  static const bool off = getenv("TR_NO_PANEL_MMA") != nullptr;
+  if (off || m > 1024 || b > 8 || rows == nullptr) return -1;
+  PanelMmaArgs pa;
+  pa.m = m;
+  pa.n = n;
+  pa.b = b;
+  pa.S = panel_mma_slot(m);
+  pa.nst = 2;
+  pa.nchunks = cdiv(n, kPmCols);
+  if (MODE == 0) {
+    const int64_t total = pa.nchunks * kPmCols * b;
+    launch("sketch_rows", k_sketch_rows, (unsigned)std::min<int64_t>(cdiv(total, 256), 4 * num_sms()),
+           256, 0, st, n, b, sk, gover, rows);
+  }
+  const float* cf = MODE == 0 ? rows : nullptr;
+  return m <= 512 ? panel_mma_launch<1, MODE>(A, P, cf, pa, partial, st)
+                  : panel_mma_launch<2, MODE>(A, P, cf, pa, partial, st);
+}
+
+template <int MODE>
+static int64_t panel_mma(const double*, int64_t, int64_t, int, const double*, const double*,
+                         SketchSpec, double*, double*, cudaStream_t) {
+  return -1;
+}
+
 template <typename T, int MODE>
 static int64_t panel(const T* A, int64_t m, int64_t n, int b, const T* P, const T* gover,
-                     SketchSpec sk, double* partial, cudaStream_t st) {
+                     SketchSpec sk, T* rows, double* partial, cudaStream_t st) {
+  const int64_t np = panel_mma<MODE>(A, m, n, b, P, gover, sk, rows, partial, st);
+  if (np >= 0) return np;
   PanelArgs pa;
   pa.m = m;
   pa.n = n;
@@ -378,14 +435,14 @@ static int bki_mode(const Shape& sh, const T* A, int64_t m, int64_t n, int r, in
                     int64_t* info, cudaStream_t st) {
   const int s = (q + 1) * b;
   const bool fused = panel_ok<T>(A, m, b);
-  int64_t np = fused ? panel<T, 0>(A, m, n, b, nullptr, gover, sk, bf.partial, st)
+  int64_t np = fused ? panel<T, 0>(A, m, n, b, nullptr, gover, sk, bf.coef, bf.partial, st)
                      : rank_update<T>(A, m, n, b, nullptr, gover, sk, bf.partial, st);
   reduce(bf.partial, np, m * b, bf.K, st);
   if (allreduce(sh, bf.K, m * b, st)) return 1;  // columns are sharded: sum the ranks
   launch("normalize_piece", k_normalize_piece<T>, 1, 1024, 0, st, bf.K, m * b, bf.P);
   for (int k = 1; k <= q; ++k) {
     if (fused) {
-      np = panel<T, 1>(A, m, n, b, bf.P, nullptr, sk, bf.partial, st);
+      np = panel<T, 1>(A, m, n, b, bf.P, nullptr, sk, bf.coef, bf.partial, st);
     } else {
       dot_cols<T>(A, m, n, bf.P, b, bf.coef, st);
       np = rank_update<T>(A, m, n, b, bf.coef, nullptr, sk, bf.partial, st);

@@ -3,6 +3,7 @@
 //   mode 0: 2-D tensor boxes {32 rows x BOXC cols} of a column-major m x n fp32
 //           matrix, 128B swizzle (the projection kernel's A tile shape)
 //   mode 1: 1-D cp.async.bulk of contiguous BYTES-sized chunks
+//   mode 2: the same chunk as separate 4 KB bulk copies (mode 3: into 4128 B slots)
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/tma_bw tools/tma_bw.cu
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -50,9 +51,14 @@ __global__ void __launch_bounds__(64, 1) k_tma(const __grid_constant__ CUtensorM
         const int k0 = (int)((b % kt) * 32), c0 = (int)((b / kt) * boxc);
         asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
                      ::"r"(dst), "l"((uint64_t)&map), "r"(k0), "r"(c0), "r"(su32(&full[st])) : "memory");
-      } else {
+      } else if (mode == 1) {
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                      ::"r"(dst), "l"(src + b * (int64_t)bytes), "r"(bytes), "r"(su32(&full[st])) : "memory");
+      } else {  // mode 2 / 3: the stage as separate 4 KB column copies, dense / 4128 B slots
+        const uint32_t slot = mode == 2 ? 4096u : 4128u;
+        for (uint32_t o = 0, k = 0; o < bytes; o += 4096, ++k)
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                       ::"r"(dst + k * slot), "l"(src + b * (int64_t)bytes + o), "r"(4096), "r"(su32(&full[st])) : "memory");
       }
     }
   } else if (threadIdx.x == 32) {
@@ -93,7 +99,7 @@ int main() {
     }
     const int64_t nboxes = mode == 0 ? (n / boxc) * (m / 32) : (m * n * 4) / bytes;
     const int stages = (stages_kb * 1024) / (int)bytes;
-    size_t smem = (size_t)stages * bytes + 1024;
+    size_t smem = (size_t)stages * bytes * 33 / 32 + 1024;
     auto go = [&](auto kern) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       for (int rep = 0; rep < 2; ++rep) {
@@ -110,6 +116,7 @@ int main() {
       case 6: go(k_tma<6>); break;
       case 8: go(k_tma<8>); break;
       case 12: go(k_tma<12>); break;
+      case 16: go(k_tma<16>); break;
       default: go(k_tma<16>); smem = 16 * bytes + 1024; break;
     }
     float ms;
@@ -124,5 +131,11 @@ int main() {
   run("bulk 16 KB contiguous", 1, 0, 16384, 192);
   run("bulk 16 KB contiguous", 1, 0, 16384, 96);
   run("bulk 48 KB contiguous", 1, 0, 49152, 192);
+  run("bulk 64 KB contiguous", 1, 0, 65536, 192);
+  run("bulk 64 KB stage as 16 x 4 KB", 2, 0, 65536, 192);
+  run("bulk 64 KB stage as 16 x 4 KB (2 st)", 2, 0, 65536, 128);
+  run("bulk 32 KB stage as 8 x 4 KB", 2, 0, 32768, 192);
+  run("bulk 32 KB stage as 8 x 4 KB, 4128 B slots", 3, 0, 32768, 192);
+  run("bulk 32 KB stage as 8 x 4 KB, 4128 B slots", 3, 0, 32768, 128);
   return 0;
 }
