@@ -180,6 +180,9 @@ int tr_profile_enable(int on);
 /* Synchronise the recorded events and aggregate them per kernel category:
  * writes up to max_entries totals (ms) and launch counts, and the category
  * names joined by '\n' into `names`.  Returns the number of categories. */
+/* Per-launch timeline of the profiled region (diagnostics; not in the reference). */
+int tr_profile_timeline(char* names, int64_t names_len, double* t0, double* t1, int64_t* streams,
+                        int max_entries);
 int tr_profile_read(char* names, int64_t names_len, double* ms, int64_t* counts,
                     int max_entries);
 

@@ -14,6 +14,7 @@
 #include "jacobi.cuh"
 #include "panel.cuh"
 #include "panel_mma.cuh"
+#include "orth_cluster.cuh"
 #include "proj_tc.cuh"
 #include "prof.cuh"
 
@@ -338,6 +339,18 @@ static TsqrPlan tsqr_plan(int64_t m, int s) {
 
 template <typename T>
 static void orth_basis(int64_t m, int s, Bufs<T>& bf, int64_t* info, cudaStream_t st) {
+  static const bool cluster_off = getenv("TR_NO_ORTH_CLUSTER") != nullptr;
+  if (!cluster_off && m <= (int64_t)kOcCtas * kOcThreads && s <= kOcS) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_orth_cluster<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)kOcSmem);
+      attr = true;
+    }
+    launch("orth", k_orth_cluster<T>, kOcCtas, kOcThreads, kOcSmem, st, (const double*)bf.K, m, s,
+           bf.Z, bf.Zt, info);
+    return;
+  }
   const TsqrPlan p = tsqr_plan(m, s);
   if (!p.ok) {
     launch("orth", k_orth<T>, 1, 1024, 0, st, bf.K, m, s, bf.work, bf.Z, bf.Zt, info);
@@ -948,6 +961,32 @@ int tr_profile_enable(int on) {
   p.records.clear();
   p.enabled = on != 0;
   return 0;
+}
+
+// Per-launch timeline of the recorded region (not cleared): category names
+// ('\n'-joined), start / end in ms relative to the first launch, stream handle.
+int tr_profile_timeline(char* names, int64_t names_len, double* t0, double* t1, int64_t* streams,
+                        int max_entries) {
+  tr::Profiler& p = tr::profiler();
+  std::lock_guard<std::mutex> g(p.mu);
+  std::string joined;
+  int n = 0;
+  for (auto& r : p.records) {
+    if (n >= max_entries) break;
+    TR_CUDA(cudaEventSynchronize(r.b));
+    float a = 0.f, b = 0.f;
+    TR_CUDA(cudaEventElapsedTime(&a, p.records[0].a, r.a));
+    TR_CUDA(cudaEventElapsedTime(&b, p.records[0].a, r.b));
+    t0[n] = a;
+    t1[n] = b;
+    streams[n] = (int64_t)(uintptr_t)r.st;
+    joined += r.cat;
+    joined += '\n';
+    ++n;
+  }
+  if ((int64_t)joined.size() + 1 > names_len) return -1;
+  memcpy(names, joined.c_str(), joined.size() + 1);
+  return n;
 }
 
 int tr_profile_read(char* names, int64_t names_len, double* ms, int64_t* counts,

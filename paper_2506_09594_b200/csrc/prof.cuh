@@ -19,6 +19,7 @@ namespace tr {
 struct ProfRecord {
   const char* cat;
   cudaEvent_t a, b;
+  cudaStream_t st;
 };
 
 struct Profiler {
@@ -52,7 +53,7 @@ inline void launch(const char* cat, K kernel, dim3 grid, dim3 block, size_t smem
   p.launches.fetch_add(1, std::memory_order_relaxed);
   if (p.enabled) {
     std::lock_guard<std::mutex> g(p.mu);
-    ProfRecord r{cat, p.get(), p.get()};
+    ProfRecord r{cat, p.get(), p.get(), st};
     cudaEventRecord(r.a, st);
     kernel<<<grid, block, smem, st>>>(args...);
     cudaEventRecord(r.b, st);
