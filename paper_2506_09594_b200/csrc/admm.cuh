@@ -729,9 +729,20 @@ static int admm_create(const AdmmConfig& cfg, int order, const int64_t* dims, co
     s->ws.push_back(p);
   }
   TR_CUDA(cudaStreamSynchronize(0));
+  // Staggered stream priorities for the per-mode LRTA chains (first mode
+  // highest), so one chain's latency kernels are dispatched ahead of the other
+  // chains' streaming blocks whenever SMs free up (TR_NO_MODE_PRIORITY: off).
+  static const bool prio = getenv("TR_NO_MODE_PRIORITY") == nullptr;
+  int least = 0, greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&least, &greatest);
   for (int k = 0; k <= nm; ++k) {
     cudaStream_t st;
-    TR_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    if (prio && k > 0) {
+      const int p = std::max(greatest, std::min(least, greatest + (k - 1)));
+      TR_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, p));
+    } else {
+      TR_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    }
     s->streams.push_back(st);
     if (k < nm) {
       cudaEvent_t e;
