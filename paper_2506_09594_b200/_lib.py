@@ -60,6 +60,8 @@ SIGNATURES = {
     "tr_gradsys_destroy": (ctypes.c_int, [_vp]),
     "tr_launch_count": (ctypes.c_int64, []),
     "tr_profile_enable": (ctypes.c_int, [ctypes.c_int]),
+    "tr_profile_timeline": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int64, _c_dp, _c_dp, _c_i64p,
+                                           ctypes.c_int]),
     "tr_profile_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int64, _c_dp, _c_i64p,
                                        ctypes.c_int]),
     "tr_prox": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double,

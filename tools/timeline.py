@@ -38,9 +38,6 @@ N = 4096
 names = ctypes.create_string_buffer(1 << 17)
 t0, t1 = (ctypes.c_double * N)(), (ctypes.c_double * N)()
 st = (ctypes.c_int64 * N)()
-lib.tr_profile_timeline.argtypes = [ctypes.c_char_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_double),
-                                    ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64),
-                                    ctypes.c_int]
 k = lib.tr_profile_timeline(names, 1 << 17, t0, t1, st, N)
 cats = names.value.decode().split("\n")[:k]
 lib.tr_profile_enable(0)
