@@ -340,7 +340,7 @@ static TsqrPlan tsqr_plan(int64_t m, int s) {
 template <typename T>
 static void orth_basis(int64_t m, int s, Bufs<T>& bf, int64_t* info, cudaStream_t st) {
   static const bool cluster_off = getenv("TR_NO_ORTH_CLUSTER") != nullptr;
-  if (!cluster_off && m <= (int64_t)kOcCtas * kOcThreads && s <= kOcS) {
+  if (!cluster_off && m <= (int64_t)kOcCtas * kOcRows && s <= kOcS) {
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(k_orth_cluster<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,

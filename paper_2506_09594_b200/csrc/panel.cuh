@@ -214,7 +214,8 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
           }
         }
         const T sum = warp_transpose_reduce32(v);
-        red[warp * (cc * B) + g0 * B + lane] = (g0 * B + lane < cc * B) ? sum : T(0);
+        // cc need not be a multiple of CPG (fp64, m = 1024: cc = 6): no store past this warp's row
+        if (g0 * B + lane < cc * B) red[warp * (cc * B) + g0 * B + lane] = sum;
       }
       __syncthreads();
       for (int e = tid; e < cc * B; e += kPanelThreads) {
