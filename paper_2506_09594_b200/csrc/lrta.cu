@@ -113,6 +113,8 @@ struct Bufs {
   double* core;
   cplx *cf0, *cf1, *U;
   int64_t* info;
+  unsigned int* ticket;  // last-block counter of k_reduce_normalize (zeroed per t-SVT)
+  double* bsum;          // its per-block sums of squares
   double *tq_tau, *tq_R, *tq_C;
   float *zhi, *zlo;
   int64_t max_parts, max_mparts;
@@ -168,6 +170,8 @@ static void carve(Carve& cv, const Shape& sh, Bufs<T>& b) {
   for (int i = 0; i < sh.tr.nt; ++i) usz += sh.tr.d[i] * sh.tr.d[i];
   b.U = cv.take<cplx>(usz);
   b.info = cv.take<int64_t>(8);
+  b.ticket = cv.take<unsigned int>(8);
+  b.bsum = cv.take<double>(cdiv(mmax * bmax, 32) + 32);
   int64_t tq = 0;
   for (int64_t mm : {sh.n1, sh.n2})
     for (int64_t ss : {sh.s0, sh.s1}) tq = std::max<int64_t>(tq, cdiv(mm, std::max<int64_t>(ss, 1)) + 1);
@@ -448,11 +452,24 @@ static int bki_mode(const Shape& sh, const T* A, int64_t m, int64_t n, int r, in
                     int64_t* info, cudaStream_t st) {
   const int s = (q + 1) * b;
   const bool fused = panel_ok<T>(A, m, b);
+  // reduce + normalise in one launch unless the columns are sharded (the
+  // all-reduce goes between the two)
+  const bool fuse_norm = sh.coll == nullptr && getenv("TR_NO_FUSED_NORMALIZE") == nullptr;
+  if (fuse_norm) TR_CUDA(cudaMemsetAsync(bf.ticket, 0, sizeof(unsigned int), st));
+  auto reduce_normalize = [&](int64_t np_, double* slot) -> int {
+    if (fuse_norm) {
+      launch("reduce_partials", k_reduce_normalize<T>, (unsigned)cdiv(m * b, 32), 256, 0, st,
+             (const double*)bf.partial, (int)np_, m * b, slot, bf.P, bf.bsum, bf.ticket);
+      return 0;
+    }
+    reduce(bf.partial, np_, m * b, slot, st);
+    if (allreduce(sh, slot, m * b, st)) return 1;  // columns are sharded: sum the ranks
+    launch("normalize_piece", k_normalize_piece<T>, 1, 1024, 0, st, slot, m * b, bf.P);
+    return 0;
+  };
   int64_t np = fused ? panel<T, 0>(A, m, n, b, nullptr, gover, sk, bf.coef, bf.partial, st)
                      : rank_update<T>(A, m, n, b, nullptr, gover, sk, bf.partial, st);
-  reduce(bf.partial, np, m * b, bf.K, st);
-  if (allreduce(sh, bf.K, m * b, st)) return 1;  // columns are sharded: sum the ranks
-  launch("normalize_piece", k_normalize_piece<T>, 1, 1024, 0, st, bf.K, m * b, bf.P);
+  if (reduce_normalize(np, bf.K)) return 1;
   for (int k = 1; k <= q; ++k) {
     if (fused) {
       np = panel<T, 1>(A, m, n, b, bf.P, nullptr, sk, bf.coef, bf.partial, st);
@@ -461,9 +478,7 @@ static int bki_mode(const Shape& sh, const T* A, int64_t m, int64_t n, int r, in
       np = rank_update<T>(A, m, n, b, bf.coef, nullptr, sk, bf.partial, st);
     }
     double* slot = bf.K + m * (int64_t)b * k;
-    reduce(bf.partial, np, m * b, slot, st);
-    if (allreduce(sh, slot, m * b, st)) return 1;
-    launch("normalize_piece", k_normalize_piece<T>, 1, 1024, 0, st, slot, m * b, bf.P);
+    if (reduce_normalize(np, slot)) return 1;
   }
   orth_basis<T>(m, s, bf, info, st);
   if (!project(A, m, n, s, bf, st)) {

@@ -214,6 +214,65 @@ __global__ void __launch_bounds__(256) k_reduce_partials(const double* __restric
   }
 }
 
+// k_reduce_partials + k_normalize_piece in one launch (the Krylov step's
+// tail, sketch.py:257-258): block b sums the partials of elements
+// [32 b, 32 b + 32) in the same order as k_reduce_partials, stores them and its
+// sum of squares; the last block to finish (ticket counter, reset by it)
+// adds the block sums in index order and scales every element by 1/||K||_F.
+// One launch instead of two per Krylov step; deterministic.
+template <typename T>
+__global__ void __launch_bounds__(256) k_reduce_normalize(const double* __restrict__ part,
+                                                          int nparts, int64_t len,
+                                                          double* __restrict__ kslot,
+                                                          T* __restrict__ p,
+                                                          double* __restrict__ bsum,
+                                                          unsigned int* __restrict__ ticket) {
+  __shared__ double acc[8][32];
+  __shared__ bool last;
+  __shared__ double inv_s;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t e = (int64_t)blockIdx.x * 32 + lane;
+  double s = 0.0;
+  if (e < len)
+    for (int q = warp; q < nparts; q += 8) s += part[(int64_t)q * len + e];
+  acc[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0) {
+    double t = 0.0;
+    if (e < len) {
+#pragma unroll
+      for (int w = 0; w < 8; ++w) t += acc[w][lane];
+      kslot[e] = t;
+    }
+    const double sq = warp_sum(t * t);
+    if (lane == 0) {
+      bsum[blockIdx.x] = sq;
+      __threadfence();
+      last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (warp == 0) {
+    double t = 0.0;
+    for (int b = lane; b < (int)gridDim.x; b += 32) t += bsum[b];
+    t = warp_sum(t);
+    if (lane == 0) {
+      const double nrm = sqrt(t);
+      inv_s = nrm > 0.0 ? 1.0 / nrm : 0.0;
+      *ticket = 0u;
+    }
+  }
+  __syncthreads();
+  const double inv = inv_s;
+  for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
+    const double v = inv > 0.0 ? __ldcg(kslot + i) * inv : __ldcg(kslot + i);
+    kslot[i] = v;
+    p[i] = (T)v;
+  }
+}
+
 // Fast fp64 reciprocal / reciprocal square root: fp32 seed + two Newton steps
 // (~1 ulp; the IEEE-rounded slow paths dominate Jacobi round latency otherwise).
 // Valid for |x| in the fp32 normal range, which the callers guarantee.
