@@ -567,7 +567,7 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
   }
   const int64_t nfa = sh.faces_all();
   const int64_t total = face * nfa;
-  const unsigned g = (unsigned)cdiv(total, 256);
+  const unsigned g = (unsigned)cdiv(4 * total, 256);  // 4 lanes per output
   // forward: mode products along trailing modes 2..d-1
   const void* src = bf.core;
   int src_real = 1;
@@ -624,7 +624,7 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
 template <typename T>
 static int expand(const Shape& sh, Bufs<T>& bf, T* out, cudaStream_t st) {
   const int64_t N = sh.n2 * sh.nf;
-  launch("expand_mode1", k_expand_mode1<T>, (unsigned)cdiv(sh.r0 * N, 256), 256, 0, st,
+  launch("expand_mode1", k_expand_mode1<T>, (unsigned)(cdiv(sh.n2, 128) * sh.nf), 128, 0, st,
          (const double*)(bf.core + sh.r0 * sh.r1 * sh.f0), (int)sh.r0, (int)sh.r1, sh.nf, bf.F1,
          sh.n2, bf.C1);
   constexpr int RA = 8, CB = sizeof(T) == 4 ? 16 : 8;

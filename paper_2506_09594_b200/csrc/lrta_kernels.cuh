@@ -761,17 +761,37 @@ __global__ void __launch_bounds__(256) k_core_from_w(const T* __restrict__ W, in
 }
 
 // C1[a + r0*(i2 + n2*f)] = sum_b core[a + r0*(b + r1*f)] * F1[i2 + n2*b]
+// C1 (r0 x n2 x nf) = core x_1 F1: C1[a, i2, f] = sum_b core[a, b, f] F1[i2, b]
+// (the mode-1 expansion ahead of k_gemm_expand, sketch.py:61).  One thread per
+// (i2, f) column of C1: the face's r0 x r1 core block sits in shared memory
+// (one block of 128 columns shares a face), the thread keeps its r0 outputs in
+// registers, reads its r1 values of F1 once (coalesced over i2) and writes a
+// contiguous column.  r0 <= 64.
 template <typename T>
-__global__ void k_expand_mode1(const double* __restrict__ core, int r0, int r1, int64_t nf,
-                               const double* __restrict__ F1, int64_t n2, T* __restrict__ C1) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (int64_t)r0 * n2 * nf) return;
-  const int a = (int)(t % r0);
-  const int64_t rest = t / r0;
-  const int64_t i2 = rest % n2, f = rest / n2;
-  double acc = 0.0;
-  for (int b = 0; b < r1; ++b) acc += core[a + (int64_t)r0 * (b + (int64_t)r1 * f)] * F1[i2 + n2 * b];
-  C1[t] = (T)acc;
+__global__ void __launch_bounds__(128) k_expand_mode1(const double* __restrict__ core, int r0,
+                                                      int r1, int64_t nf,
+                                                      const double* __restrict__ F1, int64_t n2,
+                                                      T* __restrict__ C1) {
+  __shared__ double cs[64 * 64];
+  const int64_t tiles = (n2 + 127) / 128;
+  const int64_t f = blockIdx.x / tiles;
+  const int64_t i2 = (blockIdx.x % tiles) * 128 + threadIdx.x;
+  for (int e = threadIdx.x; e < r0 * r1; e += blockDim.x) cs[e] = core[e + (int64_t)r0 * r1 * f];
+  __syncthreads();
+  if (i2 >= n2 || f >= nf) return;
+  double acc[64];
+#pragma unroll
+  for (int a = 0; a < 64; ++a) acc[a] = 0.0;
+  for (int b = 0; b < r1; ++b) {
+    const double fv = F1[i2 + n2 * b];
+#pragma unroll
+    for (int a = 0; a < 64; ++a)
+      if (a < r0) acc[a] += cs[a + r0 * b] * fv;
+  }
+  T* out = C1 + (int64_t)r0 * (i2 + n2 * f);
+#pragma unroll
+  for (int a = 0; a < 64; ++a)
+    if (a < r0) out[a] = (T)acc[a];
 }
 
 // out (n1 x N, col-major) = F0 (n1 x K) * C1 (K x N); K <= 64.
