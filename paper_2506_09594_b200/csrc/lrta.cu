@@ -115,6 +115,8 @@ struct Bufs {
   int64_t* info;
   unsigned int* ticket;  // last-block counter of k_reduce_normalize (zeroed per t-SVT)
   double* bsum;          // its per-block sums of squares
+  double* rpv;           // k_ritz_apply per-block column candidates (value, row)
+  int64_t* rpi;
   double *tq_tau, *tq_R, *tq_C;
   float *zhi, *zlo;
   int64_t max_parts, max_mparts;
@@ -172,6 +174,8 @@ static void carve(Carve& cv, const Shape& sh, Bufs<T>& b) {
   b.info = cv.take<int64_t>(8);
   b.ticket = cv.take<unsigned int>(8);
   b.bsum = cv.take<double>(cdiv(mmax * bmax, 32) + 32);
+  b.rpv = cv.take<double>((cdiv(mmax, 32) + 1) * 32);
+  b.rpi = cv.take<int64_t>((cdiv(mmax, 32) + 1) * 32);
   int64_t tq = 0;
   for (int64_t mm : {sh.n1, sh.n2})
     for (int64_t ss : {sh.s0, sh.s1}) tq = std::max<int64_t>(tq, cdiv(mm, std::max<int64_t>(ss, 1)) + 1);
@@ -455,7 +459,7 @@ static int bki_mode(const Shape& sh, const T* A, int64_t m, int64_t n, int r, in
   // reduce + normalise in one launch unless the columns are sharded (the
   // all-reduce goes between the two)
   const bool fuse_norm = sh.coll == nullptr && getenv("TR_NO_FUSED_NORMALIZE") == nullptr;
-  if (fuse_norm) TR_CUDA(cudaMemsetAsync(bf.ticket, 0, sizeof(unsigned int), st));
+  TR_CUDA(cudaMemsetAsync(bf.ticket, 0, 2 * sizeof(unsigned int), st));  // last-block tickets
   auto reduce_normalize = [&](int64_t np_, double* slot) -> int {
     if (fuse_norm) {
       launch("reduce_partials", k_reduce_normalize<T>, (unsigned)cdiv(m * b, 32), 256, 0, st,
@@ -503,8 +507,13 @@ static int bki_mode(const Shape& sh, const T* A, int64_t m, int64_t n, int r, in
     }
     launch("ritz", k_ritz_warp<T>, 1, 256, sm, st, bf.M, s, bf.Z, m, r, V, F, Ft, info);
   } else {
+    // Jacobi in one CTA; F = Z V_top and the canonical signs over many CTAs
+    const bool split = s <= 32 && r <= 32 && getenv("TR_NO_RITZ_APPLY") == nullptr;
     launch("ritz", k_ritz<T>, 1, 256, 2 * 64 * 65 * sizeof(double), st, bf.M, s, bf.Z, m, r, V,
-           F, Ft, info);
+           split ? (double*)nullptr : F, Ft, info);
+    if (split)
+      launch("ritz", k_ritz_apply<T>, (unsigned)cdiv(m, 32), 256, 0, st, (const double*)bf.Z, m,
+             s, V, r, (const int64_t*)info, F, Ft, bf.rpv, bf.rpi, bf.ticket + 1);
   }
   TR_LAUNCH_CHECK();
   return 0;

@@ -447,11 +447,15 @@ __global__ void __launch_bounds__(1024) k_orth(const double* __restrict__ K, int
   if (threadIdx.x == 0) info[0] = s_eff;
 }
 
+#ifdef TR_RITZ_PROBE
+__device__ long long g_ritz_probe[4];
+#endif
+
 // Rayleigh-Ritz (sketch.py:261-265): eigenvectors of M = W^T W by parallel
 // cyclic Jacobi, descending order, F = Z V; then the canonical sign (largest
 // |entry| of every factor column positive, first index on ties).
 template <typename T>
-__global__ void __launch_bounds__(512) k_ritz(const double* __restrict__ Mfull, int s,
+__global__ void __launch_bounds__(256) k_ritz(const double* __restrict__ Mfull, int s,
                                               const double* __restrict__ Z, int64_t m, int r,
                                               double* __restrict__ V, double* __restrict__ F,
                                               T* __restrict__ Ft, int64_t* __restrict__ info) {
@@ -482,6 +486,9 @@ __global__ void __launch_bounds__(512) k_ritz(const double* __restrict__ Mfull, 
     if (a != b) diag2 += A[a + ld * b] * A[a + ld * b];
   }
   const double mnorm = sqrt(block_sum(diag2, red));
+#ifdef TR_RITZ_PROBE
+  long long t_j0 = clock64();
+#endif
   if (ne <= 32 && blockDim.x >= 256) {
     // n <= 32: fixed roles, decoded once -- thread t owns the 2x2 block
     // (t >> 4, t & 15) of the round's J^T A J and the Q row pairs
@@ -647,6 +654,9 @@ __global__ void __launch_bounds__(512) k_ritz(const double* __restrict__ Mfull, 
       if (!any) break;
     }
   }
+#ifdef TR_RITZ_PROBE
+  if (threadIdx.x == 0) g_ritz_probe[0] = clock64() - t_j0;
+#endif
   // descending order (stable on ties, like reversing eigh's ascending output)
   if (threadIdx.x == 0) {
     for (int i = 0; i < n; ++i) {
@@ -665,6 +675,15 @@ __global__ void __launch_bounds__(512) k_ritz(const double* __restrict__ Mfull, 
   }
   __syncthreads();
   const int re = min(r, n);
+  if (n <= 32 && r <= 32 && F == nullptr) {
+    // F, its canonical signs and V's signs come from k_ritz_apply (many CTAs)
+    for (int e = threadIdx.x; e < s * r; e += blockDim.x) {
+      const int j = e % s, k = e / s;
+      V[e] = (k < re && j < n) ? Q[j + ld * order[k]] : 0.0;
+    }
+    if (threadIdx.x == 0) info[1] = re;
+    return;
+  } else {
   // F = Z V (m x r): one row of Z per thread, held in registers (independent loads)
   for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
     if (n <= 32) {
@@ -693,6 +712,9 @@ __global__ void __launch_bounds__(512) k_ritz(const double* __restrict__ Mfull, 
     }
   }
   __syncthreads();
+#ifdef TR_RITZ_PROBE
+  if (threadIdx.x == 0) g_ritz_probe[1] = clock64() - t_j0;
+#endif
   // canonical sign: one warp per column, argmax |F| with first-index ties
   {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -720,6 +742,7 @@ __global__ void __launch_bounds__(512) k_ritz(const double* __restrict__ Mfull, 
       if (lane == 0) sgn[k] = bval < 0.0 ? -1.0 : 1.0;
     }
   }
+  }  // n > 32 or r > 32
   __syncthreads();
   for (int64_t e = threadIdx.x; e < m * r; e += blockDim.x) {
     const double f = F[e] * sgn[e / m];
@@ -731,6 +754,116 @@ __global__ void __launch_bounds__(512) k_ritz(const double* __restrict__ Mfull, 
     V[e] = (k < re && j < n) ? Q[j + ld * order[k]] * sgn[k] : 0.0;
   }
   if (threadIdx.x == 0) info[1] = re;
+#ifdef TR_RITZ_PROBE
+  if (threadIdx.x == 0) g_ritz_probe[2] = clock64() - t_j0;
+#endif
+}
+
+// Rayleigh-Ritz factor F = Z V_top (m x r, n, r <= 32) and its canonical sign
+// (largest-|entry| of every column positive, first index on ties), spread
+// over CTAs of 32 rows: each CTA forms its rows and a per-column argmax; the
+// last CTA (ticket) combines them in row-block order, flips V's columns and
+// rescales F / Ft.  V holds V_top (s x r, unsigned) on entry, signed on exit.
+template <typename T>
+__global__ void __launch_bounds__(256) k_ritz_apply(const double* __restrict__ Z, int64_t m, int s,
+                                                    double* __restrict__ V, int r,
+                                                    const int64_t* __restrict__ info,
+                                                    double* __restrict__ F, T* __restrict__ Ft,
+                                                    double* __restrict__ pbv,
+                                                    int64_t* __restrict__ pbi,
+                                                    unsigned int* __restrict__ ticket) {
+  __shared__ double zs[32][33];
+  __shared__ double vs[32][33];
+  __shared__ double sg[32];
+  __shared__ bool last;
+  const int n = (int)info[0];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t r0 = (int64_t)blockIdx.x * 32;
+  for (int e = tid; e < 32 * 32; e += blockDim.x) {
+    const int i = e & 31, j = e >> 5;
+    zs[i][j] = (r0 + i < m && j < n) ? Z[r0 + i + m * j] : 0.0;
+    vs[i][j] = (i < n && j < r) ? V[i + (int64_t)s * j] : 0.0;  // vs[j_row][k_col]
+  }
+  __syncthreads();
+  // thread (row lane, columns warp + 8 c): rows of this block, 4 columns each
+  const int64_t row = r0 + lane;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int k = warp + 8 * c;
+    double f = 0.0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) f += zs[lane][j] * vs[j][k];
+    if (row < m && k < r) F[row + m * k] = f;
+    // warp argmax over the block's 32 rows (first index on ties)
+    double b = (row < m) ? f : 0.0;
+    int64_t ix = (row < m) ? row : INT64_MAX;
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, b, o);
+      const int64_t oi = __shfl_xor_sync(0xffffffffu, ix, o);
+      if (fabs(ob) > fabs(b) || (fabs(ob) == fabs(b) && oi < ix)) {
+        b = ob;
+        ix = oi;
+      }
+    }
+    if (lane == 0 && k < r) {
+      pbv[(int64_t)blockIdx.x * 32 + k] = b;
+      pbi[(int64_t)blockIdx.x * 32 + k] = ix;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // column k: combine the blocks' candidates, 8 threads per column
+  {
+    const int k = tid >> 3, part = tid & 7;
+    double b = 0.0;
+    int64_t ix = INT64_MAX;
+    if (k < r)
+      for (int64_t q = part; q < (int64_t)gridDim.x; q += 8) {
+        const double ob = __ldcg(pbv + q * 32 + k);
+        const int64_t oi = __ldcg(pbi + q * 32 + k);
+        if (fabs(ob) > fabs(b) || (fabs(ob) == fabs(b) && oi < ix)) {
+          b = ob;
+          ix = oi;
+        }
+      }
+    for (int o = 4; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, b, o);
+      const int64_t oi = __shfl_xor_sync(0xffffffffu, ix, o);
+      if (fabs(ob) > fabs(b) || (fabs(ob) == fabs(b) && oi < ix)) {
+        b = ob;
+        ix = oi;
+      }
+    }
+    if (part == 0 && k < 32) sg[k] = b < 0.0 ? -1.0 : 1.0;
+  }
+  __syncthreads();
+  for (int e = tid; e < s * r; e += blockDim.x) V[e] *= sg[e / s];
+  // F / Ft rescale, 8 independent loads in flight per thread
+  const int64_t tot = m * r;
+  for (int64_t e0 = tid; e0 < tot; e0 += 8 * (int64_t)blockDim.x) {
+    double fv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t e = e0 + (int64_t)u * blockDim.x;
+      fv[u] = e < tot ? __ldcg(F + e) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t e = e0 + (int64_t)u * blockDim.x;
+      if (e < tot) {
+        const double f = fv[u] * sg[e / m];
+        F[e] = f;
+        Ft[e] = (T)f;
+      }
+    }
+  }
+  if (tid == 0) *ticket = 0u;
 }
 
 // core rows from W: out[lo + inner*(i + r*f)] = sum_j W[c*s + j] V[j + s*i],
