@@ -611,8 +611,12 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
     launch("face_svt", k_face_svt_warp, (unsigned)cdiv(nfa, 4), 128, sm, st, (double2*)faces,
            (int)sh.r0, (int)sh.r1, nfa, pen, tau);
   } else {
-    launch("face_svt", k_face_svt, (unsigned)nfa, 1024, smem, st, faces, (int)sh.r0,
-           (int)sh.r1, pen, tau);
+    // one warp per Jacobi pair: no idle warps at the per-round barrier
+    static const int fth_env = getenv("TR_FACE_THREADS") ? atoi(getenv("TR_FACE_THREADS")) : 0;
+    const int npairs = (int)((sh.r1 + (sh.r1 & 1)) / 2);
+    const int fth = fth_env > 0 ? fth_env : std::min(1024, std::max(128, 32 * npairs));
+    launch("face_svt", k_face_svt, (unsigned)nfa, fth, smem, st, faces, (int)sh.r0, (int)sh.r1,
+           pen, tau);
   }
   if (kind == TR_TRANSFORM_FFT) launch("mirror_fix", k_mirror_fix, g, 256, 0, st, faces, face, nfa, sh.tr);
   // inverse: U^H / alpha in reverse mode order, real part on the last step
