@@ -660,9 +660,9 @@ static int admm_create(const AdmmConfig& cfg, int order, const int64_t* dims, co
       return 1;
     }
   } else {
-    if (!(dims[0] <= 64 && dims[1] <= 64)) {
+    if (!(dims[0] <= 4096 && dims[1] <= 4096)) {
       delete s;
-      TR_REQUIRE(false, "deterministic t-SVT on the GPU needs face slices up to 64 x 64; "
+      TR_REQUIRE(false, "deterministic t-SVT on the GPU needs face slices up to 4096 x 4096; "
                         "use the randomized solver for larger tensors");
     }
     Shape& f = s->sh;

@@ -86,15 +86,14 @@ __global__ void k_mode_product(const void* __restrict__ in_, int in_real, void* 
 }
 
 // One CTA per face: X (r0 x r1 complex, column-major at faces + f*r0*r1) is
-// replaced by U prox(S) V^H.  r0, r1 <= 64.
-__global__ void __launch_bounds__(1024) k_face_svt(cplx* __restrict__ faces, int r0, int r1,
-                                                    Penalty pen, double tau) {
-  extern __shared__ double svt_smem[];
-  cplx* X = reinterpret_cast<cplx*>(svt_smem);  // r0 x r1, ld = r0
-  cplx* V = X + r0 * r1;                        // r1 x r1, ld = r1
+// replaced by U prox(S) V^H (one-sided Jacobi).  The working copy X and the
+// rotations V live in shared memory (r0, r1 <= 64: k_face_svt) or in global
+// scratch (larger faces, the deterministic t-SVT of a whole tensor:
+// k_face_svt_g); wsc holds r1 weights.
+__device__ inline void face_svt_body(cplx* __restrict__ X, cplx* __restrict__ V,
+                                     double* __restrict__ wsc, cplx* __restrict__ src, int r0,
+                                     int r1, Penalty pen, double tau) {
   __shared__ int rot_any;
-  __shared__ double wsc[64];
-  cplx* src = faces + (int64_t)blockIdx.x * r0 * r1;
   for (int e = threadIdx.x; e < r0 * r1; e += blockDim.x) X[e] = src[e];
   for (int e = threadIdx.x; e < r1 * r1; e += blockDim.x)
     V[e] = {(e % r1) == (e / r1) ? 1.0 : 0.0, 0.0};
@@ -184,6 +183,25 @@ __global__ void __launch_bounds__(1024) k_face_svt(cplx* __restrict__ faces, int
     }
     src[e] = {ar, ai};
   }
+}
+
+__global__ void __launch_bounds__(1024) k_face_svt(cplx* __restrict__ faces, int r0, int r1,
+                                                    Penalty pen, double tau) {
+  extern __shared__ double svt_smem[];
+  cplx* X = reinterpret_cast<cplx*>(svt_smem);  // r0 x r1, ld = r0
+  cplx* V = X + r0 * r1;                        // r1 x r1, ld = r1
+  __shared__ double wsc[64];
+  face_svt_body(X, V, wsc, faces + (int64_t)blockIdx.x * r0 * r1, r0, r1, pen, tau);
+}
+
+// faces larger than 64: X / V in global scratch (xw: faces-sized, vw: r1^2 per face)
+__global__ void __launch_bounds__(1024) k_face_svt_g(cplx* __restrict__ faces, cplx* __restrict__ xw,
+                                                      cplx* __restrict__ vw, int r0, int r1,
+                                                      Penalty pen, double tau) {
+  extern __shared__ double wsc_g[];  // r1 weights
+  const int64_t f = blockIdx.x;
+  face_svt_body(xw + f * r0 * r1, vw + f * (int64_t)r1 * r1, wsc_g, faces + f * r0 * r1, r0, r1,
+                pen, tau);
 }
 
 // FFT faces: every non-canonical face (mirror < f) becomes conj(face[mirror]).

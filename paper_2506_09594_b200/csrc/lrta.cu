@@ -112,6 +112,7 @@ struct Bufs {
   T *F0t, *F1t, *A1, *C1;
   double* core;
   cplx *cf0, *cf1, *U;
+  cplx* fv;  // face-SVT rotations for faces larger than 64 (global scratch)
   int64_t* info;
   unsigned int* ticket;  // last-block counter of k_reduce_normalize (zeroed per t-SVT)
   double* bsum;          // its per-block sums of squares
@@ -168,6 +169,7 @@ static void carve(Carve& cv, const Shape& sh, Bufs<T>& b) {
   b.core = cv.take<double>(sh.r0 * sh.r1 * sh.faces_all());
   b.cf0 = cv.take<cplx>(sh.r0 * sh.r1 * sh.faces_all());
   b.cf1 = cv.take<cplx>(sh.r0 * sh.r1 * sh.faces_all());
+  b.fv = cv.take<cplx>(sh.r0 > 64 || sh.r1 > 64 ? sh.r1 * sh.r1 * sh.faces_all() : 0);
   int64_t usz = 0;
   for (int i = 0; i < sh.tr.nt; ++i) usz += sh.tr.d[i] * sh.tr.d[i];
   b.U = cv.take<cplx>(usz);
@@ -600,7 +602,12 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
                                  2 * 64 * 64 * (int)sizeof(cplx)));
     attr = true;
   }
-  if (sh.r0 <= kJW && sh.r1 <= kJW && g_use_warp_jacobi) {
+  if (sh.r0 > 64 || sh.r1 > 64) {
+    // large faces (deterministic t-SVT of a whole tensor): X / V in global scratch,
+    // X in the free mode-product buffer
+    launch("face_svt", k_face_svt_g, (unsigned)nfa, 1024, (size_t)sh.r1 * sizeof(double), st,
+           faces, bufs[cur], bf.fv, (int)sh.r0, (int)sh.r1, pen, tau);
+  } else if (sh.r0 <= kJW && sh.r1 <= kJW && g_use_warp_jacobi) {
     const size_t sm = 4 * 4 * kJW * kVld * sizeof(double);
     static bool wattr = false;
     if (!wattr) {

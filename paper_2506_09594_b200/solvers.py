@@ -132,9 +132,9 @@ class NativeSolver:
             _, ranks, blocks, krylov = _resolve(cfg.sketch, dims)
             seed = cfg.sketch.seed
         else:
-            if dims[0] > 64 or dims[1] > 64:
+            if dims[0] > 4096 or dims[1] > 4096:
                 raise NotImplementedError(
-                    "the deterministic t-SVT runs on the B200 for face slices up to 64 x 64; "
+                    "the deterministic t-SVT runs on the B200 for face slices up to 4096 x 4096; "
                     "set randomized=True with a SketchConfig for larger tensors")
             ranks, blocks, krylov, seed = (1, 1), (1, 1), (0, 0), 0
         tcode, tmats, talphas, self._tkeep = transform.device_args(dims)

@@ -144,3 +144,27 @@ def test_zero_problem_converges_immediately(cuda_lib):
     l, e, rep = pk.gnrhtc(np.zeros((6, 5, 4)), mask, pk.SolverConfig(max_iters=5))
     assert rep.converged and rep.iterations == 1
     assert not l.any() and not e.any()
+
+
+def test_deterministic_large_faces_match_oracle(cuda_lib):
+    """Deterministic GNRHTC (the reference's default, randomized=False) with
+    face slices larger than 64 x 64: the face SVT keeps its working copy and
+    rotations in global scratch (k_face_svt_g).  96 x 80 x 6, 4 sweeps, fp64."""
+    import paper_2506_09594_b200 as pk
+    from oracle.tensor_ops import mode_product
+    rng = np.random.default_rng(9)
+    core = rng.standard_normal((5, 5, 6))
+    x = mode_product(mode_product(core, rng.standard_normal((96, 5)), 0),
+                     rng.standard_normal((80, 5)), 1)
+    mask = rng.random(x.shape) < 0.6
+    mobs = np.where(mask, x, 0.0)
+    l, e, rep = pk.gnrhtc(mobs, mask, pk.SolverConfig(max_iters=4))
+    spec = TransformSpec("fft")
+    mcp = (2, 2.5, 0.0)
+    lo, eo, hist = admm.admm_complete(mobs, mask, lambda a, tau: lrta.gnhtsvt(a, spec, mcp, tau),
+                                      mcp, admm.default_lambda(mobs.shape), (0, 1, 2),
+                                      max_iters=4)
+    assert np.linalg.norm(l - lo) / np.linalg.norm(lo) <= 1e-9
+    assert np.linalg.norm(e - eo) / max(np.linalg.norm(eo), 1e-300) <= 1e-9
+    np.testing.assert_allclose(np.array(rep.residual_history), np.array(hist["residuals"]),
+                               rtol=1e-6, atol=1e-9)
