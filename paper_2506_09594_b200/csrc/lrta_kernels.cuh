@@ -266,10 +266,22 @@ __global__ void __launch_bounds__(256) k_reduce_normalize(const double* __restri
   }
   __syncthreads();
   const double inv = inv_s;
-  for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
-    const double v = inv > 0.0 ? __ldcg(kslot + i) * inv : __ldcg(kslot + i);
-    kslot[i] = v;
-    p[i] = (T)v;
+  for (int64_t i0 = threadIdx.x; i0 < len; i0 += 8 * (int64_t)blockDim.x) {
+    double v[8];  // 8 independent loads in flight before the stores
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t i = i0 + (int64_t)u * blockDim.x;
+      v[u] = i < len ? __ldcg(kslot + i) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t i = i0 + (int64_t)u * blockDim.x;
+      if (i < len) {
+        const double x = inv > 0.0 ? v[u] * inv : v[u];
+        kslot[i] = x;
+        p[i] = (T)x;
+      }
+    }
   }
 }
 

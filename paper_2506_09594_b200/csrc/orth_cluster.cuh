@@ -26,6 +26,14 @@
 
 namespace tr {
 
+#ifdef TR_ORTH_PROBE
+__device__ long long g_orth_probe[8];
+#define OC_MARK(i) \
+  if (threadIdx.x == 0 && cl.block_rank() == 0) g_orth_probe[i] = clock64() - oc_t0;
+#else
+#define OC_MARK(i)
+#endif
+
 constexpr int kOcThreads = 512;  // 16 warps
 constexpr int kOcWarps = kOcThreads / 32;
 constexpr int kOcRows = 256;          // rows per CTA
@@ -178,6 +186,9 @@ __global__ void __cluster_dims__(kOcCtas, 1, 1) __launch_bounds__(kOcThreads, 1)
   const int64_t row0 = (int64_t)c * kOcRows;
   const int64_t left = m - row0;
   const int rows_c = left <= 0 ? 0 : (left < kOcRows ? (int)left : kOcRows);
+#ifdef TR_ORTH_PROBE
+  const long long oc_t0 = clock64();
+#endif
   // cluster-wide "all CTAs running" before the first remote shared-memory store
   asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 
@@ -193,6 +204,7 @@ __global__ void __cluster_dims__(kOcCtas, 1, 1) __launch_bounds__(kOcThreads, 1)
     }
   }
   col_householder<kOcRpl>(a, rows_c, s, colk, gk, tau);
+  OC_MARK(0)
   const int kloc = rows_c < s ? rows_c : s;
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
@@ -212,6 +224,7 @@ __global__ void __cluster_dims__(kOcCtas, 1, 1) __launch_bounds__(kOcThreads, 1)
     }
   }
   cl.sync();
+  OC_MARK(1)
 
   if (c == 0) {
     // ---- 2. QR of the stack (kOcCtas*s x s) ----
@@ -243,6 +256,7 @@ __global__ void __cluster_dims__(kOcCtas, 1, 1) __launch_bounds__(kOcThreads, 1)
       }
     }
     const double tol = 1e-14 * sqrt(block_sum(f, bscr));  // barriers: rp, stk ready
+    OC_MARK(2)
     // ---- 3. pivoted QR of R (one warp) ----
     if (warp == 0) {
       int se = s;
@@ -315,6 +329,7 @@ __global__ void __cluster_dims__(kOcCtas, 1, 1) __launch_bounds__(kOcThreads, 1)
       if (lane == 0) se_s = se;
     }
     __syncthreads();
+    OC_MARK(3)
     const int se = se_s;
     // ---- 4. C = Q_stack [E; 0] (kOcCtas*s x se); rows -> the owning CTAs ----
     double cc[2][RS];
@@ -328,6 +343,7 @@ __global__ void __cluster_dims__(kOcCtas, 1, 1) __launch_bounds__(kOcThreads, 1)
       }
     }
     col_apply_q<RS>(stk, kOcStack, nst, nst < s ? nst : s, taut, cc, se);
+    OC_MARK(4)
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       const int j = warp + kOcWarps * q;
@@ -345,6 +361,7 @@ __global__ void __cluster_dims__(kOcCtas, 1, 1) __launch_bounds__(kOcThreads, 1)
   }
   cl.sync();
 
+  OC_MARK(5)
   // ---- 5. Z rows of this CTA = Q_c [C_c; 0] ----
   const int se = se_s;
   double zz[2][kOcRpl];
@@ -358,6 +375,7 @@ __global__ void __cluster_dims__(kOcCtas, 1, 1) __launch_bounds__(kOcThreads, 1)
     }
   }
   col_apply_q<kOcRpl>(vloc, kOcRows, rows_c, kloc, tau, zz, se);
+  OC_MARK(6)
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
     const int j = warp + kOcWarps * q;
