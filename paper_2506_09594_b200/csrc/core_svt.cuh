@@ -85,6 +85,25 @@ __global__ void k_mode_product(const void* __restrict__ in_, int in_real, void* 
   else ((cplx*)out_)[t] = {ar, ai};
 }
 
+// FFT faces: every non-canonical face (mirror < f) becomes conj(face[mirror]).
+// trailing dims t[0..nt) column-major flattening (tenrec/transform.py:169-183).
+struct Trailing {
+  int nt;
+  int64_t d[8];
+};
+
+__device__ __forceinline__ int64_t mirror_face(int64_t f, const Trailing& tr) {
+  int64_t out = 0, mul = 1, rem = f;
+  for (int i = 0; i < tr.nt; ++i) {
+    const int64_t n = tr.d[i];
+    const int64_t t = rem % n;
+    rem /= n;
+    out += ((n - t) % n) * mul;
+    mul *= n;
+  }
+  return out;
+}
+
 // One CTA per face: X (r0 x r1 complex, column-major at faces + f*r0*r1) is
 // replaced by U prox(S) V^H (one-sided Jacobi).  The working copy X and the
 // rotations V live in shared memory (r0, r1 <= 64: k_face_svt) or in global
@@ -185,8 +204,16 @@ __device__ inline void face_svt_body(cplx* __restrict__ X, cplx* __restrict__ V,
   }
 }
 
+// skip (FFT transforms, mirror_tr.nt > 0): faces whose mirror is an earlier
+// face are overwritten by k_mirror_fix, so their CTAs exit at once and leave
+// the SMs to the other mode streams.
+__device__ __forceinline__ bool face_is_mirror_copy(int64_t f, const Trailing& mirror_tr) {
+  return mirror_tr.nt > 0 && mirror_face(f, mirror_tr) < f;
+}
+
 __global__ void __launch_bounds__(1024) k_face_svt(cplx* __restrict__ faces, int r0, int r1,
-                                                    Penalty pen, double tau) {
+                                                    Penalty pen, double tau, Trailing mirror_tr) {
+  if (face_is_mirror_copy(blockIdx.x, mirror_tr)) return;
   extern __shared__ double svt_smem[];
   cplx* X = reinterpret_cast<cplx*>(svt_smem);  // r0 x r1, ld = r0
   cplx* V = X + r0 * r1;                        // r1 x r1, ld = r1
@@ -197,30 +224,12 @@ __global__ void __launch_bounds__(1024) k_face_svt(cplx* __restrict__ faces, int
 // faces larger than 64: X / V in global scratch (xw: faces-sized, vw: r1^2 per face)
 __global__ void __launch_bounds__(1024) k_face_svt_g(cplx* __restrict__ faces, cplx* __restrict__ xw,
                                                       cplx* __restrict__ vw, int r0, int r1,
-                                                      Penalty pen, double tau) {
+                                                      Penalty pen, double tau, Trailing mirror_tr) {
+  if (face_is_mirror_copy(blockIdx.x, mirror_tr)) return;
   extern __shared__ double wsc_g[];  // r1 weights
   const int64_t f = blockIdx.x;
   face_svt_body(xw + f * r0 * r1, vw + f * (int64_t)r1 * r1, wsc_g, faces + f * r0 * r1, r0, r1,
                 pen, tau);
-}
-
-// FFT faces: every non-canonical face (mirror < f) becomes conj(face[mirror]).
-// trailing dims t[0..nt) column-major flattening (tenrec/transform.py:169-183).
-struct Trailing {
-  int nt;
-  int64_t d[8];
-};
-
-__device__ __forceinline__ int64_t mirror_face(int64_t f, const Trailing& tr) {
-  int64_t out = 0, mul = 1, rem = f;
-  for (int i = 0; i < tr.nt; ++i) {
-    const int64_t n = tr.d[i];
-    const int64_t t = rem % n;
-    rem /= n;
-    out += ((n - t) % n) * mul;
-    mul *= n;
-  }
-  return out;
 }
 
 __global__ void k_mirror_fix(cplx* __restrict__ faces, int64_t face_len, int64_t nf, Trailing tr) {

@@ -595,6 +595,9 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
     st_lo *= n;
   }
   cplx* faces = (cplx*)src;
+  // FFT: only canonical faces are factored (the rest are mirrored afterwards)
+  Trailing mirror_tr = sh.tr;
+  if (kind != TR_TRANSFORM_FFT || getenv("TR_ALL_FACES") != nullptr) mirror_tr.nt = 0;
   const size_t smem = (size_t)(face + sh.r1 * sh.r1) * sizeof(cplx);
   static bool attr = false;
   if (!attr) {
@@ -606,7 +609,7 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
     // large faces (deterministic t-SVT of a whole tensor): X / V in global scratch,
     // X in the free mode-product buffer
     launch("face_svt", k_face_svt_g, (unsigned)nfa, 1024, (size_t)sh.r1 * sizeof(double), st,
-           faces, bufs[cur], bf.fv, (int)sh.r0, (int)sh.r1, pen, tau);
+           faces, bufs[cur], bf.fv, (int)sh.r0, (int)sh.r1, pen, tau, mirror_tr);
   } else if (sh.r0 <= kJW && sh.r1 <= kJW && g_use_warp_jacobi) {
     const size_t sm = 4 * 4 * kJW * kVld * sizeof(double);
     static bool wattr = false;
@@ -623,7 +626,7 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
     const int npairs = (int)((sh.r1 + (sh.r1 & 1)) / 2);
     const int fth = fth_env > 0 ? fth_env : std::min(1024, std::max(128, 32 * npairs));
     launch("face_svt", k_face_svt, (unsigned)nfa, fth, smem, st, faces, (int)sh.r0, (int)sh.r1,
-           pen, tau);
+           pen, tau, mirror_tr);
   }
   if (kind == TR_TRANSFORM_FFT) launch("mirror_fix", k_mirror_fix, g, 256, 0, st, faces, face, nfa, sh.tr);
   // inverse: U^H / alpha in reverse mode order, real part on the last step
