@@ -365,8 +365,8 @@ static int full_svt(Solver<T>& s, const T* X, T* out, double tau, void* ws, cuda
   return 0;
 }
 
-template <typename T>
-static int low_rank_step(Solver<T>& s, double tau) {
+template <typename T, typename F>
+static int low_rank_step(Solver<T>& s, double tau, F&& on_main) {
   // fork: each mode on its own stream after the main stream's LRTA inputs
   // (TR_SERIAL_MODES: all on the main stream, for uncontended kernel timings)
   static const bool serial = getenv("TR_SERIAL_MODES") != nullptr;
@@ -384,8 +384,14 @@ static int low_rank_step(Solver<T>& s, double tau) {
     if (rc) return rc;
     TR_CUDA(cudaEventRecord(s.evs[k], sk));
   }
+  on_main();  // work of the main stream that overlaps the per-mode chains
   for (int k = 0; k < s.cfg.nmodes; ++k) TR_CUDA(cudaStreamWaitEvent(s.streams[0], s.evs[k], 0));
   return 0;
+}
+
+template <typename T>
+static int low_rank_step(Solver<T>& s, double tau) {
+  return low_rank_step<T>(s, tau, [] {});
 }
 
 // residual slots written by a step (host array of TR_ADMM_NOUT doubles)
@@ -484,6 +490,7 @@ static int admm_step(Solver<T>& s, double* hout) {
   const int64_t rb = grid;
   // slots in res: [0..4] lag of mode k (5 each, up to 10 modes) | [64..70] noise/dual | [80..] onebit
   double tau;
+  bool overlap_noise = false;
   if (!s.onebit()) {
     // L-subproblem (solvers.py:231-233)
     if (pure) {
@@ -495,21 +502,29 @@ static int admm_step(Solver<T>& s, double* hout) {
     }
     tau = 1.0 / (gamma * mu);
     lrta_inputs<T>(s, s.l, mu, v4, grid, st);
-    if (low_rank_step<T>(s, tau)) return 2;
-    if (!fuse) lag_updates<T>(s, s.l, mu, v4, grid, st);
     // noise and dual updates (solvers.py:239-246)
     const double level = s.cfg.lam / mu;
     const int structure = s.cfg.kind == 1 ? 3 : s.cfg.structure;
     const double q0 = s.cfg.psi.p0, q1 = s.cfg.psi.p1;
-    if (structure == 1 || structure == 2) {
-      const int64_t face = g.dims[0] * g.dims[1];
-      const unsigned gg = (unsigned)(structure == 1 ? cdiv(face, 256) : N / face);
+    // E', Y' need only L: with TR_OVERLAP_NOISE they run on the main stream
+    // while the per-mode t-SVTs run and the fused tail reads them instead of
+    // recomputing them.  Off by default: on the bench workload the extra
+    // streaming blocks delay the mode chains' latency kernels more than the
+    // shorter tail saves (9.62 vs 9.31 ms per sweep).
+    static const bool overlap_env = getenv("TR_OVERLAP_NOISE") != nullptr;
+    const bool overlap = fuse && overlap_env;
+    overlap_noise = overlap;
+    auto group_scale = [&] {
+      if (structure == 1 || structure == 2) {
+        const int64_t face = g.dims[0] * g.dims[1];
+        const unsigned gg = (unsigned)(structure == 1 ? cdiv(face, 256) : N / face);
 #define TR_GS(K)                                                                             \
   launch("group_scale", k_group_scale<T, K>, gg, 256, 0, st, g, structure, s.A, s.mask,     \
          (const T*)s.l, (const T*)s.y, mu, q0, q1, level, s.scale)
-      TR_PEN_DISPATCH(s.cfg.psi.kind, TR_GS)
+        TR_PEN_DISPATCH(s.cfg.psi.kind, TR_GS)
 #undef TR_GS
-    }
+      }
+    };
 #define TR_ND2(K, S)                                                                          \
   launch("noise_dual", v4 ? k_noise_dual<T, K, S, 4> : k_noise_dual<T, K, S, 1>, grid,        \
          kRedThreads, 0, st, g, s.A, s.mask,                                                   \
@@ -522,6 +537,18 @@ static int admm_step(Solver<T>& s, double* hout) {
     case 2: TR_ND2(K, 2); break;            \
     default: TR_ND2(K, 3); break;           \
   }
+    auto noise_dual = [&] {
+      group_scale();
+      TR_PEN_DISPATCH(s.cfg.psi.kind, TR_ND)
+      launch("final_reduce", k_final_reduce, 1, 256, 0, st, (const double*)part, (int)rb, 7,
+             0b0010101u, res + 64);
+    };
+    if (low_rank_step<T>(s, tau, [&] {
+          if (overlap) noise_dual();
+        }))
+      return 2;
+    if (!fuse) lag_updates<T>(s, s.l, mu, v4, grid, st);
+    if (!overlap && fuse) group_scale();
     if (fuse) {
       ModePtrs<T> gn{}, go{}, lw{};
       gn.count = go.count = lw.count = nm;
@@ -533,11 +560,17 @@ static int admm_step(Solver<T>& s, double* hout) {
       }
       const double mu_next = std::min(s.cfg.mu_max, s.cfg.growth * mu);
       unsigned tgrid = 0;
-#define TR_ST2(K, S)                                                                            \
-  tgrid = resident_grid(k_sweep_tail<T, K, S>, N);                                              \
-  launch("sweep_tail", k_sweep_tail<T, K, S>, tgrid, kRedThreads, 0, st, g, s.A, s.mask,        \
+#define TR_ST3(K, S, NZ)                                                                        \
+  tgrid = resident_grid(k_sweep_tail<T, K, S, NZ>, N);                                          \
+  launch("sweep_tail", k_sweep_tail<T, K, S, NZ>, tgrid, kRedThreads, 0, st, g, s.A, s.mask,    \
          (const T*)s.l, (const T*)s.lold, s.e, s.y, gn, go, lp, lw, mu, mu_next, q0, q1, level, \
          (const double*)s.scale, s.rhs, part)
+#define TR_ST2(K, S)        \
+  if (overlap) {            \
+    TR_ST3(K, S, false);    \
+  } else {                  \
+    TR_ST3(K, S, true);     \
+  }
 #define TR_ST(K)                 \
   switch (structure) {           \
     case 0: TR_ST2(K, 0); break; \
@@ -548,6 +581,7 @@ static int admm_step(Solver<T>& s, double* hout) {
       TR_PEN_DISPATCH(s.cfg.psi.kind, TR_ST)
 #undef TR_ST
 #undef TR_ST2
+#undef TR_ST3
       // partial slots: 5 per mode (4 slots) then the 7 noise values -> res[96..122]
       launch("final_reduce", k_final_reduce, 1, 256, 0, st, (const double*)part, (int)tgrid, 27,
              0b0010101u << 20 | 0b00101u | 0b00101u << 5 | 0b00101u << 10 | 0b00101u << 15,
@@ -555,9 +589,7 @@ static int admm_step(Solver<T>& s, double* hout) {
       for (int k = 0; k < nm; ++k) std::swap(s.lag[k], s.lag2[k]);
       s.rhs_ready = true;
     } else {
-      TR_PEN_DISPATCH(s.cfg.psi.kind, TR_ND)
-      launch("final_reduce", k_final_reduce, 1, 256, 0, st, (const double*)part, (int)rb, 7,
-             0b0010101u, res + 64);
+      noise_dual();
     }
 #undef TR_ND
 #undef TR_ND2
@@ -596,7 +628,7 @@ static int admm_step(Solver<T>& s, double* hout) {
   TR_CUDA(cudaStreamSynchronize(st));
   const double* h = s.hres;
   const double* hl = fuse ? h + 96 : h;          // per-mode multiplier residuals
-  const double* hn = fuse ? h + 96 + 20 : h + 64;  // noise / dual residuals
+  const double* hn = (fuse && !overlap_noise) ? h + 96 + 20 : h + 64;  // noise / dual residuals
   for (int i = 0; i < R_NOUT; ++i) hout[i] = 0.0;
   double grad = 0, dg = 0, dgf = 0, gradf = 0, lagn = 0;
   for (int k = 0; k < nm; ++k) {

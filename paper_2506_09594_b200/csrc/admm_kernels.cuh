@@ -489,7 +489,10 @@ __global__ void __launch_bounds__(kRedThreads) k_noise_dual(Geom g, const T* __r
 // at ip with the very expression the owner of ip evaluates, so rhs' is
 // bit-identical to k_admm_rhs of the next sweep.  Partials per block: 5 per
 // mode slot (k_lag_update's, 4 slots) then the 7 of k_noise_dual.
-template <typename T, int KIND, int STRUCT>
+// NOISE = false: E' and Y' were already written in place by k_noise_dual
+// (launched on the main stream while the per-mode t-SVTs ran); the pass reads
+// them instead of recomputing them and leaves the 7 noise partials at zero.
+template <typename T, int KIND, int STRUCT, bool NOISE = true>
 __global__ void __launch_bounds__(kRedThreads, 1) k_sweep_tail(
     Geom g, const T* __restrict__ mobs, const uint8_t* __restrict__ mask, const T* __restrict__ l,
     const T* __restrict__ lold, T* __restrict__ e, T* __restrict__ y, ModePtrs<T> gn, ModePtrs<T> go,
@@ -512,10 +515,11 @@ __global__ void __launch_bounds__(kRedThreads, 1) k_sweep_tail(
     const int64_t base = lc.line * n0, i = base + i0;
     // ---- every load of the chunk first (memory-level parallelism) ----
     const Vec<T, V> lv = ldv_nc<T, V>(l + i), mv = ldv_nc<T, V>(mobs + i);
-    const Vec<T, V> ov = ldv_nc<T, V>(lold + i);
+    Vec<T, V> ov;
+    if (NOISE) ov = ldv_nc<T, V>(lold + i);
     const Vec<T, V> yv = ldv<T, V>(y + i), ev = ldv<T, V>(e + i);
     bool obs[V];
-    ld_mask<V>(mask + i, obs);
+    if (NOISE) ld_mask<V>(mask + i, obs);
     Vec<T, V> gnv[MM], gov[MM], lgv[MM], lnx[MM], lpv[MM], gpv[MM], mpv[MM];
 #pragma unroll
     for (int k = 0; k < MM; ++k) {
@@ -543,8 +547,17 @@ __global__ void __launch_bounds__(kRedThreads, 1) k_sweep_tail(
     }
     // ---- noise and dual (k_noise_dual) ----
     T en[V], yn[V], acc[V];
+    if (!NOISE) {
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        en[j] = ev.x[j];  // already E', Y'
+        yn[j] = yv.x[j];
+        acc[j] = (mv.x[j] - en[j]) + yn[j] * imu2;
+      }
+    }
 #pragma unroll
     for (int j = 0; j < V; ++j) {
+      if (!NOISE) break;
       const T mi = mv.x[j], li = lv.x[j], yi = yv.x[j];
       const T h = mi - li + yi * timu;
       T ej;
@@ -571,8 +584,10 @@ __global__ void __launch_bounds__(kRedThreads, 1) k_sweep_tail(
       vn[6] += yn[j] * yn[j];
       acc[j] = (mi - ej) + yn[j] * imu2;  // b' = A - E' + Y' / mu'
     }
-    stv<T, V>(e + i, en);
-    stv<T, V>(y + i, yn);
+    if (NOISE) {
+      stv<T, V>(e + i, en);
+      stv<T, V>(y + i, yn);
+    }
     // ---- multipliers (k_lag_update) and the next rhs (k_admm_rhs) ----
 #pragma unroll
     for (int k = 0; k < MM; ++k) {
