@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(kPwThreads, 1)
   const int64_t iters = my_tiles * kt;
 
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
         smem_u32(&tmem_base_s)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -176,12 +176,16 @@ __global__ void __launch_bounds__(kPwThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer ----
+      // A x [Z_hi | Z_lo] as ONE N = 64 MMA (the two Z tiles sit next to each
+      // other: 64 K-major rows), A_lo x Z_hi as an N = 32 MMA into the first
+      // half: A is read from shared memory twice per K-step instead of three times
+      const uint32_t idesc64 = idesc_tf32(128, 64);
       const uint32_t idesc = idesc_tf32(128, 32);
       for (int64_t t = 0; t < my_tiles; ++t) {
         const int acc = (int)(t & 1);
         mbar_wait(&tempty[acc], (uint32_t)(((t >> 1) & 1) ^ 1));
         tc_fence_after();
-        const uint32_t d = tmem + (uint32_t)(acc * 32);
+        const uint32_t d = tmem + (uint32_t)(acc * 64);
         for (int kk = 0; kk < kt; ++kk) {
           const int64_t it = t * kt + kk;
           const int st = (int)(it % kPwStages);
@@ -193,12 +197,10 @@ __global__ void __launch_bounds__(kPwThreads, 1)
           const uint64_t dAl =
               umma_desc_sw128(sbase + (uint32_t)(kPwStages * kPwStageBytes + ls * kPjTileBytes));
           const uint64_t dZh = umma_desc_sw128(sa + kPjTileBytes);
-          const uint64_t dZl = umma_desc_sw128(sa + kPjTileBytes + kPjZBytes);
 #pragma unroll
           for (int k = 0; k < 4; ++k) {  // K = 8 per MMA: +32 B in the swizzled row
             const uint64_t adv = (uint64_t)(2 * k);
-            umma_tf32(d, dA + adv, dZh + adv, idesc, (kk == 0 && k == 0) ? 0u : 1u);
-            umma_tf32(d, dA + adv, dZl + adv, idesc, 1u);
+            umma_tf32(d, dA + adv, dZh + adv, idesc64, (kk == 0 && k == 0) ? 0u : 1u);
             umma_tf32(d, dAl + adv, dZh + adv, idesc, 1u);
           }
           umma_commit(&empty[st]);
@@ -242,8 +244,11 @@ __global__ void __launch_bounds__(kPwThreads, 1)
       const int acc = (int)(t & 1);
       mbar_wait(&tfull[acc], (uint32_t)((t >> 1) & 1));
       tc_fence_after();
-      float w[32];
-      tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * 32), w);
+      float w[32], wl[32];
+      tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * 64), w);
+      tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * 64 + 32), wl);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) w[j] += wl[j];  // A Z_hi + A_lo Z_hi + A Z_lo
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
       const int64_t col = (blockIdx.x + t * gridDim.x) * 128 + row;
@@ -275,7 +280,7 @@ __global__ void __launch_bounds__(kPwThreads, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
   }
 }
 
