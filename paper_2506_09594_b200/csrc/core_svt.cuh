@@ -42,49 +42,6 @@ __global__ void k_build_transform(int kind, int n, cplx* __restrict__ U) {
   }
 }
 
-// out[lo + st*(k + n*hi)] = sum_j M(k, j) in[lo + st*(j + n*hi)] with
-// M = U (inverse = 0) or U^H / alpha (inverse = 1).  `in_real` reads a real
-// input; `out_real` writes the real part only.  Four lanes per output split
-// the j sum (j = sub, sub + 4, ...) and combine it with two xor shuffles in a
-// fixed order: 4x the parallelism and a 4x shorter dependent chain for the
-// small core transforms (n = transform length, total = core size).
-__global__ void k_mode_product(const void* __restrict__ in_, int in_real, void* __restrict__ out_,
-                               int out_real, int64_t st, int n, int64_t hi_count,
-                               const cplx* __restrict__ U, int inverse, double alpha) {
-  const int64_t tq = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int sub = (int)(tq & 3);
-  const int64_t t = tq >> 2;
-  const int64_t total = st * n * hi_count;
-  const bool live = t < total;
-  const int64_t tt = live ? t : 0;
-  const int64_t lo = tt % st;
-  const int k = (int)((tt / st) % n);
-  const int64_t hi = tt / (st * n);
-  double ar = 0.0, ai = 0.0;
-  if (live) {
-    for (int j = sub; j < n; j += 4) {
-      cplx u = inverse ? cconj(U[j * n + k]) : U[k * n + j];
-      const int64_t src = lo + st * (j + (int64_t)n * hi);
-      cplx x;
-      if (in_real) x = {((const double*)in_)[src], 0.0};
-      else x = ((const cplx*)in_)[src];
-      ar += u.re * x.re - u.im * x.im;
-      ai += u.re * x.im + u.im * x.re;
-    }
-  }
-  ar += __shfl_xor_sync(0xffffffffu, ar, 1);
-  ai += __shfl_xor_sync(0xffffffffu, ai, 1);
-  ar += __shfl_xor_sync(0xffffffffu, ar, 2);
-  ai += __shfl_xor_sync(0xffffffffu, ai, 2);
-  if (!live || sub != 0) return;
-  if (inverse) {
-    ar /= alpha;
-    ai /= alpha;
-  }
-  if (out_real) ((double*)out_)[t] = ar;
-  else ((cplx*)out_)[t] = {ar, ai};
-}
-
 // FFT faces: every non-canonical face (mirror < f) becomes conj(face[mirror]).
 // trailing dims t[0..nt) column-major flattening (tenrec/transform.py:169-183).
 struct Trailing {
@@ -202,6 +159,52 @@ __device__ inline void face_svt_body(cplx* __restrict__ X, cplx* __restrict__ V,
     }
     src[e] = {ar, ai};
   }
+}
+
+// out[lo + st*(k + n*hi)] = sum_j M(k, j) in[lo + st*(j + n*hi)] with
+// M = U (inverse = 0) or U^H / alpha (inverse = 1).  `in_real` reads a real
+// input; `out_real` writes the real part only.  Four lanes per output split
+// the j sum (j = sub, sub + 4, ...) and combine it with two xor shuffles in a
+// fixed order: 4x the parallelism and a 4x shorter dependent chain for the
+// small core transforms (n = transform length, total = core size).
+// skip_tr.nt > 0 (last forward FFT product): outputs of faces that the mirror
+// step overwrites afterwards are not formed (face = t / face_len).
+__global__ void k_mode_product(const void* __restrict__ in_, int in_real, void* __restrict__ out_,
+                               int out_real, int64_t st, int n, int64_t hi_count,
+                               const cplx* __restrict__ U, int inverse, double alpha,
+                               int64_t face_len, Trailing skip_tr) {
+  const int64_t tq = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int sub = (int)(tq & 3);
+  const int64_t t = tq >> 2;
+  const int64_t total = st * n * hi_count;
+  const bool live = t < total && !(skip_tr.nt > 0 && mirror_face(t / face_len, skip_tr) < t / face_len);
+  const int64_t tt = live ? t : 0;
+  const int64_t lo = tt % st;
+  const int k = (int)((tt / st) % n);
+  const int64_t hi = tt / (st * n);
+  double ar = 0.0, ai = 0.0;
+  if (live) {
+    for (int j = sub; j < n; j += 4) {
+      cplx u = inverse ? cconj(U[j * n + k]) : U[k * n + j];
+      const int64_t src = lo + st * (j + (int64_t)n * hi);
+      cplx x;
+      if (in_real) x = {((const double*)in_)[src], 0.0};
+      else x = ((const cplx*)in_)[src];
+      ar += u.re * x.re - u.im * x.im;
+      ai += u.re * x.im + u.im * x.re;
+    }
+  }
+  ar += __shfl_xor_sync(0xffffffffu, ar, 1);
+  ai += __shfl_xor_sync(0xffffffffu, ai, 1);
+  ar += __shfl_xor_sync(0xffffffffu, ar, 2);
+  ai += __shfl_xor_sync(0xffffffffu, ai, 2);
+  if (!live || sub != 0) return;
+  if (inverse) {
+    ar /= alpha;
+    ai /= alpha;
+  }
+  if (out_real) ((double*)out_)[t] = ar;
+  else ((cplx*)out_)[t] = {ar, ai};
 }
 
 // skip (FFT transforms, mirror_tr.nt > 0): faces whose mirror is an earlier

@@ -585,10 +585,15 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
   cplx* bufs[2] = {bf.cf0, bf.cf1};
   int cur = 0;
   int64_t st_lo = face;
+  Trailing no_skip = sh.tr;
+  no_skip.nt = 0;
+  Trailing fwd_skip = sh.tr;  // last forward FFT product: mirrored faces are not needed
+  if (kind != TR_TRANSFORM_FFT || getenv("TR_ALL_FACES") != nullptr) fwd_skip.nt = 0;
   for (int i = 0; i < nt; ++i) {
     const int n = (int)sh.tr.d[i];
     const int64_t hi = nfa / (st_lo / face) / n;
-    launch("mode_product", k_mode_product, g, 256, 0, st, src, src_real, bufs[cur], 0, st_lo, n, hi, U[i], 0, 1.0);
+    launch("mode_product", k_mode_product, g, 256, 0, st, src, src_real, bufs[cur], 0, st_lo, n,
+           hi, U[i], 0, 1.0, face, i == nt - 1 ? fwd_skip : no_skip);
     src = bufs[cur];
     src_real = 0;
     cur ^= 1;
@@ -636,7 +641,8 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
     const int64_t hi = nfa / (st_lo / face) / n;
     const bool last = (i == 0);
     void* dst = last ? (void*)bf.core : (void*)bufs[cur];
-    launch("mode_product", k_mode_product, g, 256, 0, st, src, 0, dst, last ? 1 : 0, st_lo, n, hi, U[i], 1, al[i]);
+    launch("mode_product", k_mode_product, g, 256, 0, st, src, 0, dst, last ? 1 : 0, st_lo, n,
+           hi, U[i], 1, al[i], face, no_skip);
     src = dst;
     cur ^= 1;
   }
