@@ -108,7 +108,7 @@ __device__ inline void face_svt_body(cplx* __restrict__ X, cplx* __restrict__ V,
         const double rg = (g2 > 1e-36 && g2 < 1e36) ? fast_rsqrt(g2) : 1.0 / sqrt(g2);
         const double g = g2 * rg;
         double c, s;
-        jacobi_cs(al, be, g, c, s);  // tau = (beta - alpha) / (2 |gamma|)
+        jacobi_cs_fast(al, be, g, c, s);  // tau = (beta - alpha) / (2 |gamma|), fp32 tangent
         const cplx ph = {gr * rg, gi * rg};  // e^{i phi}
         // [xp, xq] <- [xp, xq] [[c, s e^{i phi}], [-s e^{-i phi}, c]]
         const cplx spn = {s * ph.re, s * ph.im};   // s e^{i phi}
