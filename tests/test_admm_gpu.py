@@ -168,3 +168,6 @@ def test_deterministic_large_faces_match_oracle(cuda_lib):
     assert np.linalg.norm(e - eo) / max(np.linalg.norm(eo), 1e-300) <= 1e-9
     np.testing.assert_allclose(np.array(rep.residual_history), np.array(hist["residuals"]),
                                rtol=1e-6, atol=1e-9)
+    # the fp32 stream through the same large-face path
+    l32, e32, _ = pk.gnrhtc(mobs.astype(np.float32), mask, pk.SolverConfig(max_iters=4))
+    assert np.linalg.norm(l32 - lo) / np.linalg.norm(lo) <= 1e-4
