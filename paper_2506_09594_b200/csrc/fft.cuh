@@ -1024,12 +1024,15 @@ __global__ void __launch_bounds__(256, 3) k_fft_t(const void* in, void* out,  //
     if (mode == FFT_C2R) {
       // pair (k, NT-k): Z[k] = E + i O, Z[NT-k] = conj(E - i O) with
       // E = (X[k] + conj X[NT-k]) / 2, O = conj(w^k) (X[k] - conj X[NT-k]) / 2
-      constexpr int NIT = (NP * L + 255) / 256;
+      // warp-wide runs of 32 consecutive bins of one line: the gathers at k and
+      // NT - k and the line-major stores below stay free of bank conflicts
+      constexpr int NKB = (NP + 31) / 32;
+      constexpr int NIT = (NKB * L * 32 + 255) / 256;
       cpx<T> z1[NIT], z2[NIT];
 #pragma unroll
       for (int c = 0; c < NIT; ++c) {
         const int e = tid + c * 256;
-        const int l = e & (L - 1), k = e >> LL;
+        const int q = e >> 5, l = q & (L - 1), k = ((q >> LL) << 5) + (e & 31);
         if (k < NP) {
           const cpx<T> a = buf[fpad(l * (hn + 1) + k)];
           const cpx<T> bb = cconjt(buf[fpad(l * (hn + 1) + NT - k)]);
@@ -1044,7 +1047,7 @@ __global__ void __launch_bounds__(256, 3) k_fft_t(const void* in, void* out,  //
 #pragma unroll
       for (int c = 0; c < NIT; ++c) {
         const int e = tid + c * 256;
-        const int l = e & (L - 1), k = e >> LL;
+        const int q = e >> 5, l = q & (L - 1), k = ((q >> LL) << 5) + (e & 31);
         if (k < NP) {
           buf[fpad((l << LN) + k)] = z1[c];
           if (k > 0 && k < NT / 2) buf[fpad((l << LN) + NT - k)] = z2[c];
