@@ -114,6 +114,45 @@ int tr_rsthosvd_bki(int dtype, const void* a, int order, const int64_t* dims,
                     int64_t workspace_bytes, void* stream);
 
 /*
+ * Generic Tucker compression -- replaces tenrec.sketch.rsthosvd_bki for any
+ * processing order (sketch.py:211-270) and tenrec.sketch.ad_rsthosvd_blbp
+ * (fixed-accuracy block Lanczos bidiagonalisation, sketch.py:287-403); with
+ * tr_tucker_svt it replaces tenrec.sketch.gnhtsvt_randomized for every
+ * SketchConfig the fused tr_gnhtsvt_randomized does not take (sketch.py:406-456).
+ * Host-synchronous: returns once the factors and core are on the device.
+ *
+ *   a, order, dims   the tensor (dtype, device, column-major)
+ *   sketch_mode      0 fixed-rank (ranks/blocks/krylov per processed mode),
+ *                    1 fixed-accuracy (eps, block, defl_tol <= 0 for the default
+ *                    1e-10 ||unfolding||_F)
+ *   nproc, proc_order  the modes to compress, in processing order
+ *   seed             Philox seed: fixed-rank step p draws entry (c, t) at
+ *                    (seed, p, c*b + t); fixed-accuracy draw j (start block of a
+ *                    mode or fill block, counted in call order across modes) is
+ *                    the (n, cols) block of entries (seed, j, c*cols + t)
+ * Factor columns carry the canonical sign (largest-|entry| positive).
+ * tr_tucker_info: per mode (order entries) core dims, ranks (dims[k] for
+ * unprocessed modes), processed flags and the BLBPDiagnostics traces (energy,
+ * deflations, iterations, local orthogonality loss); any pointer may be NULL.
+ * tr_tucker_read: which = -1 copies the core (fp64, natural column-major
+ * layout), which = k the factor of mode k (fp64, dims[k] x ranks[k]).
+ * tr_tucker_svt: out (dtype, the full dims) = the transform-domain SVT of the
+ * core (transform adapted to the core's trailing sizes) re-expanded through
+ * the factors; the handle's core is not modified.
+ */
+int tr_tucker_create(int dtype, const void* a, int order, const int64_t* dims, int sketch_mode,
+                     int nproc, const int64_t* proc_order, const int64_t* ranks,
+                     const int64_t* blocks, const int64_t* krylov, double eps, int64_t block,
+                     double defl_tol, uint64_t seed, void* stream, void** handle);
+int tr_tucker_info(void* handle, int64_t* core_dims, int64_t* ranks, int64_t* processed,
+                   double* energy, int64_t* deflations, int64_t* iterations, double* orth_loss);
+int tr_tucker_read(void* handle, int which, double* dst, void* stream);
+int tr_tucker_svt(void* handle, int transform_kind, const void* transform_mats,
+                  const double* alphas, int penalty_kind, double p0, double p1, double tau,
+                  void* out, void* stream);
+int tr_tucker_destroy(void* handle);
+
+/*
  * Elementwise proximity operator -- replaces Penalty.prox(mu, v)
  * (tenrec/penalties.py:45-61) on a device array of n values (dtype).
  */
@@ -138,7 +177,8 @@ int tr_prox(int dtype, int penalty_kind, double p0, double p1, double mu, const 
  * tr_admm_step runs one sweep and writes TR_ADMM_NOUT residuals to `out`
  * (host): [dL, dE, grad_gap, dG, fit_gap, dL_fro, dE_fro, dG_fro, fit_fro,
  *  grad_gap_fro, ||Y||, max_k ||Lambda_k||, mu, rel_dL (one-bit), box_gap (one-bit)].
- * tr_admm_read copies state `which` (0 L, 1 E or S, 2 Y, 3 Z) to `dst` (device).
+ * tr_admm_read copies state `which` (0 L, 1 E or S, 2 Y, 3 Z, 4 + k the G tensor of
+ * gradient mode k, i.e. the last sweep's t-SVT output) to `dst` (device).
  */
 #define TR_ADMM_NOUT 15
 int tr_admm_create(int dtype, int order, const int64_t* dims, int kind, const void* obs_a,
@@ -152,6 +192,13 @@ int tr_admm_create(int dtype, int order, const int64_t* dims, int kind, const vo
 int tr_admm_step(void* handle, double* out);
 int tr_admm_read(void* handle, int which, void* dst, void* stream);
 int tr_admm_destroy(void* handle);
+/* Route the solver's t-SVTs through the generic Tucker engine (tr_tucker_*)
+ * with this sketch: any processing order, fixed-rank (sketch_mode 0) or
+ * fixed-accuracy block Lanczos (sketch_mode 1); arguments as tr_tucker_create.
+ * Replaces the randomized/ranks/blocks/krylov/seed of tr_admm_create. */
+int tr_admm_set_sketch(void* handle, int sketch_mode, int nproc, const int64_t* proc_order,
+                       const int64_t* ranks, const int64_t* blocks, const int64_t* krylov,
+                       double eps, int64_t block, double defl_tol, uint64_t seed);
 /* The solver's main cudaStream_t (every sweep starts and ends on it). */
 void* tr_admm_stream(void* handle);
 

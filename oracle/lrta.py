@@ -8,6 +8,7 @@ Restates tenrec/sketch.py and tenrec/shrink.py:
   rsthosvd_bki       sketch.py:211-270
   blbp_factor        sketch.py:287-352   one mode of AD-RSTHOSVD-BLBP (Algorithm 3)
   ad_rsthosvd_blbp   sketch.py:355-403
+  gnhtsvt_randomized_blbp  sketch.py:406-456 with the fixed-accuracy compression
   gnhtt              shrink.py:57-73
   gnhtsvt            shrink.py:76-106
   gnhtsvt_randomized sketch.py:430-456
@@ -175,8 +176,14 @@ def local_orthogonality_loss(blocks):
     return loss
 
 
-def blbp_factor(a, eps, b, tol, draw):
-    """One fixed-accuracy sweep; ``draw(n, cols)`` yields Gaussian blocks in order."""
+def blbp_factor(a, eps, b, tol, draw, canonical=False):
+    """One fixed-accuracy sweep; ``draw(n, cols)`` yields Gaussian blocks in order.
+
+    ``canonical`` fixes the sign of every column of the finished factor
+    (largest-|entry| positive), the convention of the GPU path: every step of
+    the bidiagonalisation is equivariant under column sign flips of its
+    blocks, so the factors then agree whatever sign convention each QR uses.
+    """
     m, n = a.shape
     norm2 = float(np.linalg.norm(a) ** 2)
     if norm2 == 0.0:
@@ -223,14 +230,37 @@ def blbp_factor(a, eps, b, tol, draw):
         if s_u == 0 or v_next.shape[1] == 0 or u_acc.shape[1] >= m:
             break
         v_cur, u_prev, l_prev = v_next, u_i, l_next
+    if canonical:
+        u_acc = canonicalize_columns(u_acc)
     return u_acc, blocks, energy, defl, it
 
 
-def ad_rsthosvd_blbp(x, eps, block=10, defl_tol=None, order=None, rng=None):
+class PhiloxDraws:
+    """The GPU path's Gaussian draws for block Lanczos: draw j of the call (a
+    mode's start block or a fill block, counted across modes) is the (n, cols)
+    Philox block of stream j (tenrec_b200.h: tr_tucker_create)."""
+
+    def __init__(self, seed):
+        from .philox import PhiloxSketchSource
+
+        self.src = PhiloxSketchSource(seed)
+        self.count = 0
+
+    def __call__(self, n, cols):
+        g = self.src.draw(self.count, n, cols)
+        self.count += 1
+        return g
+
+
+def ad_rsthosvd_blbp(x, eps, block=10, defl_tol=None, order=None, rng=None, draw=None,
+                     canonical=False):
+    """sketch.py:355-403.  ``rng`` (numpy Generator, the reference's stream) or
+    ``draw(n, cols)`` (e.g. PhiloxDraws) supplies the Gaussian blocks."""
     x = np.asarray(x, dtype=np.float64)
     order = tuple(range(x.ndim)) if order is None else tuple(order)
-    rng = np.random.default_rng(0) if rng is None else rng
-    draw = lambda n, c: rng.standard_normal((n, c))  # noqa: E731
+    if draw is None:
+        rng = np.random.default_rng(0) if rng is None else rng
+        draw = lambda n, c: rng.standard_normal((n, c))  # noqa: E731
     factors = [None] * x.ndim
     diag = {"energy": {}, "ranks": {}, "deflations": {}, "orth_loss": {}, "iterations": {}}
     core = x
@@ -238,7 +268,7 @@ def ad_rsthosvd_blbp(x, eps, block=10, defl_tol=None, order=None, rng=None):
         a = unfold(core, k)
         nrm = float(np.linalg.norm(a))
         tol = defl_tol if defl_tol is not None else 1e-10 * max(nrm, 1e-300)
-        f, blocks, energy, dfl, its = blbp_factor(a, eps, block, tol, draw)
+        f, blocks, energy, dfl, its = blbp_factor(a, eps, block, tol, draw, canonical)
         factors[k] = f
         diag["energy"][k] = energy
         diag["ranks"][k] = f.shape[1]
@@ -299,6 +329,16 @@ def gnhtsvt_randomized(a, spec, pen, tau, ranks, blocks=None, krylov=None, order
     """Tucker-compressed t-SVT (sketch.py:430-456), fixed-rank BKI compression."""
     a = np.asarray(a, dtype=np.float64)
     core, factors = rsthosvd_bki(a, ranks, order, blocks, krylov, source, canonical)
+    if any(n == 0 for n in core.shape):
+        return np.zeros(a.shape)
+    return reconstruct(gnhtsvt(core, spec, pen, tau), factors, a.shape)
+
+
+def gnhtsvt_randomized_blbp(a, spec, pen, tau, eps, block=10, defl_tol=None, order=(0, 1),
+                            rng=None, draw=None, canonical=False):
+    """Tucker-compressed t-SVT with fixed-accuracy BLBP compression (sketch.py:406-456)."""
+    a = np.asarray(a, dtype=np.float64)
+    core, factors, _ = ad_rsthosvd_blbp(a, eps, block, defl_tol, order, rng, draw, canonical)
     if any(n == 0 for n in core.shape):
         return np.zeros(a.shape)
     return reconstruct(gnhtsvt(core, spec, pen, tau), factors, a.shape)

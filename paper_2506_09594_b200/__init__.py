@@ -13,7 +13,8 @@ from .gradient import GradientSet, solve_grad_system
 from .onebit import (ObservationSet, data_fit_update, gnobhtc, gnobrhtc, naive_estimate,
                      onebit_observe)
 from .shard import DeviceAllreduce, gnhtsvt_randomized_sharded, shard_range
-from .sketch import SketchConfig, TuckerFactors, gnhtsvt_randomized, rsthosvd_bki
+from .sketch import (BLBPDiagnostics, SketchConfig, TuckerFactors, ad_rsthosvd_blbp,
+                     gnhtsvt_randomized, rsthosvd_bki)
 from .solvers import SolveReport, SolverConfig, default_lambda, gnhtc, gnrhtc
 from .transform import DEFAULT_TRANSFORM, Transform, TransformError
 
@@ -21,7 +22,8 @@ __version__ = "0.1.0"
 
 __all__ = [
     "PENALTY_NAMES", "L1", "MCP", "SCAD", "CappedLq", "Firm", "LogPenalty", "Lq", "Penalty",
-    "make_penalty", "SketchConfig", "TuckerFactors", "gnhtsvt_randomized", "rsthosvd_bki",
+    "make_penalty", "SketchConfig", "TuckerFactors", "BLBPDiagnostics", "gnhtsvt_randomized",
+    "rsthosvd_bki", "ad_rsthosvd_blbp",
     "DEFAULT_TRANSFORM", "Transform", "TransformError", "SolveReport", "SolverConfig",
     "default_lambda", "gnhtc", "gnrhtc", "ObservationSet", "data_fit_update", "gnobhtc",
     "gnobrhtc", "naive_estimate", "onebit_observe", "GradientSet", "solve_grad_system", "DeviceAllreduce", "gnhtsvt_randomized_sharded", "shard_range",

@@ -53,6 +53,9 @@ SIGNATURES = {
     "tr_admm_read": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp]),
     "tr_admm_destroy": (ctypes.c_int, [_vp]),
     "tr_admm_stream": (_vp, [_vp]),
+    "tr_admm_set_sketch": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _c_i64p, _c_i64p,
+                                          _c_i64p, _c_i64p, ctypes.c_double, ctypes.c_int64,
+                                          ctypes.c_double, ctypes.c_uint64]),
     "tr_gradsys_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _c_i64p, ctypes.c_int,
                                          ctypes.POINTER(ctypes.c_int),
                                          ctypes.POINTER(ctypes.c_void_p)]),
@@ -64,6 +67,16 @@ SIGNATURES = {
                                            ctypes.c_int]),
     "tr_profile_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int64, _c_dp, _c_i64p,
                                        ctypes.c_int]),
+    "tr_tucker_create": (ctypes.c_int, [
+        ctypes.c_int, _vp, ctypes.c_int, _c_i64p, ctypes.c_int, ctypes.c_int, _c_i64p, _c_i64p,
+        _c_i64p, _c_i64p, ctypes.c_double, ctypes.c_int64, ctypes.c_double, ctypes.c_uint64, _vp,
+        ctypes.POINTER(ctypes.c_void_p)]),
+    "tr_tucker_info": (ctypes.c_int, [_vp, _c_i64p, _c_i64p, _c_i64p, _c_dp, _c_i64p, _c_i64p,
+                                      _c_dp]),
+    "tr_tucker_read": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp]),
+    "tr_tucker_svt": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _c_dp, ctypes.c_int, ctypes.c_double,
+                                     ctypes.c_double, ctypes.c_double, _vp, _vp]),
+    "tr_tucker_destroy": (ctypes.c_int, [_vp]),
     "tr_prox": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double,
                                ctypes.c_double, _vp, _vp, ctypes.c_int64, _vp]),
 }

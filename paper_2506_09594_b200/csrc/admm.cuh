@@ -80,6 +80,8 @@ struct Solver {
   std::vector<cudaEvent_t> evs;
   cudaEvent_t ev_main = nullptr;
   SolveSpec ss;
+  bool generic = false;  // low-rank step through the generic Tucker engine (tucker.cuh)
+  TuckerSpec tspec;
   double mu;
   int64_t red_blocks;
   std::vector<void*> allocs;
@@ -365,6 +367,22 @@ static int full_svt(Solver<T>& s, const T* X, T* out, double tau, void* ws, cuda
   return 0;
 }
 
+// Tucker-compressed t-SVT of one gradient tensor through the generic engine
+// (any processing order, fixed-rank or fixed-accuracy sketch; host-driven)
+template <typename T>
+static int generic_svt(Solver<T>& s, const T* X, T* out, double tau, cudaStream_t st) {
+  TuckerResult res;
+  if (tucker_compress<T>(X, s.order, s.g.dims, s.tspec, res, st)) return 2;
+  if (res.core_size() == 0) {
+    TR_CUDA(cudaMemsetAsync(out, 0, sizeof(T) * s.g.N, st));
+    return 0;
+  }
+  if (tucker_core_svt<T>(res, res.core, s.cfg.tkind, s.cfg.tmats, s.cfg.talphas, s.cfg.phi, tau,
+                         st))
+    return 2;
+  return tucker_reconstruct<T>(res, res.core, out, st);
+}
+
 template <typename T, typename F>
 static int low_rank_step(Solver<T>& s, double tau, F&& on_main) {
   // fork: each mode on its own stream after the main stream's LRTA inputs
@@ -375,7 +393,9 @@ static int low_rank_step(Solver<T>& s, double tau, F&& on_main) {
     cudaStream_t sk = serial ? s.streams[0] : s.streams[k + 1];
     TR_CUDA(cudaStreamWaitEvent(sk, s.ev_main, 0));
     int rc;
-    if (s.cfg.randomized)
+    if (s.generic)
+      rc = generic_svt<T>(s, s.X[k], s.gnew[k], tau, sk);
+    else if (s.cfg.randomized)
       rc = gnhtsvt_randomized_t<T>(s.X[k], s.gnew[k], s.sh, s.cfg.seed, s.cfg.tkind, s.cfg.tmats,
                                    s.cfg.talphas, s.cfg.phi, tau, nullptr, nullptr, s.ws[k],
                                    s.ws_bytes, sk);

@@ -152,9 +152,6 @@ __device__ __forceinline__ int rr_player(int k, int r, int n) {
   return k == 0 ? 0 : 1 + (k - 1 + r) % (n - 1);
 }
 
-// Debug counters (sweeps of the iterative small solvers), read by tr_debug_read.
-static __device__ __managed__ int g_dbg[8];
-
 inline int num_sms() {
   static int n = 0;
   if (!n) {

@@ -129,7 +129,6 @@ __device__ inline void face_svt_body(cplx* __restrict__ X, cplx* __restrict__ V,
       }
       __syncthreads();
     }
-    if (threadIdx.x == 0) atomicAdd(&g_dbg[1], 1);  // face sweeps (summed over faces)
     if (!rot_any) break;
     __syncthreads();
   }

@@ -11,7 +11,6 @@
 #include "core_svt.cuh"
 #include "lrta_kernels.cuh"
 #include "tsqr.cuh"
-#include "jacobi.cuh"
 #include "panel.cuh"
 #include "panel_mma.cuh"
 #include "orth_cluster.cuh"
@@ -21,10 +20,6 @@
 namespace tr {
 
 static thread_local char g_err[2048] = "";
-
-// Warp-register Jacobi (jacobi.cuh) for the small SVDs; off by default: on
-// B200 it is issue-latency bound (one warp per matrix, ~4.7 cycles/issue).
-static bool g_use_warp_jacobi = getenv("TR_WARP_JACOBI") != nullptr;
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -377,7 +372,8 @@ static void orth_basis(int64_t m, int s, Bufs<T>& bf, int64_t* info, cudaStream_
   static const int tq_threads = getenv("TR_TSQR_THREADS") ? atoi(getenv("TR_TSQR_THREADS")) : 256;
   launch("orth", k_tsqr_local, p.nb, tq_threads, p.sm_local, st, bf.K, m, s, p.RB, bf.work,
          bf.tq_tau, bf.tq_R, nrows);
-  launch("orth", k_tsqr_top, 1, tq_threads, p.sm_top, st, bf.tq_R, (int)nrows, s, bf.tq_C, info);
+  launch("orth", k_tsqr_top, 1, tq_threads, p.sm_top, st, bf.tq_R, (int)nrows, s, bf.tq_C, info,
+         0.0, 1, (double*)nullptr);
   launch("orth", k_tsqr_form<T>, p.nb, tq_threads, p.sm_form, st, bf.work, bf.tq_tau, bf.tq_C,
          (int)nrows, m, s, p.RB, bf.Z, bf.Zt);
 }
@@ -500,23 +496,13 @@ static int bki_mode(const Shape& sh, const T* A, int64_t m, int64_t n, int r, in
     reduce(bf.Mpart, mp, (int64_t)s * s, bf.M, st);
   }
   if (allreduce(sh, bf.M, (int64_t)s * s, st)) return 1;  // W rows are sharded
-  if (s <= kJW && g_use_warp_jacobi) {
-    const size_t sm = 4 * kJW * kVld * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_ritz_warp<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      attr = true;
-    }
-    launch("ritz", k_ritz_warp<T>, 1, 256, sm, st, bf.M, s, bf.Z, m, r, V, F, Ft, info);
-  } else {
-    // Jacobi in one CTA; F = Z V_top and the canonical signs over many CTAs
-    const bool split = s <= 32 && r <= 32 && getenv("TR_NO_RITZ_APPLY") == nullptr;
-    launch("ritz", k_ritz<T>, 1, 256, 2 * 64 * 65 * sizeof(double), st, bf.M, s, bf.Z, m, r, V,
-           split ? (double*)nullptr : F, Ft, info);
-    if (split)
-      launch("ritz", k_ritz_apply<T>, (unsigned)cdiv(m, 32), 256, 0, st, (const double*)bf.Z, m,
-             s, V, r, (const int64_t*)info, F, Ft, bf.rpv, bf.rpi, bf.ticket + 1);
-  }
+  // Jacobi in one CTA; F = Z V_top and the canonical signs over many CTAs
+  const bool split = s <= 32 && r <= 32 && getenv("TR_NO_RITZ_APPLY") == nullptr;
+  launch("ritz", k_ritz<T>, 1, 256, 2 * 64 * 65 * sizeof(double), st, bf.M, s, bf.Z, m, r, V,
+         split ? (double*)nullptr : F, Ft, info);
+  if (split)
+    launch("ritz", k_ritz_apply<T>, (unsigned)cdiv(m, 32), 256, 0, st, (const double*)bf.Z, m,
+           s, V, r, (const int64_t*)info, F, Ft, bf.rpv, bf.rpi, bf.ticket + 1);
   TR_LAUNCH_CHECK();
   return 0;
 }
@@ -615,16 +601,6 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
     // X in the free mode-product buffer
     launch("face_svt", k_face_svt_g, (unsigned)nfa, 1024, (size_t)sh.r1 * sizeof(double), st,
            faces, bufs[cur], bf.fv, (int)sh.r0, (int)sh.r1, pen, tau, mirror_tr);
-  } else if (sh.r0 <= kJW && sh.r1 <= kJW && g_use_warp_jacobi) {
-    const size_t sm = 4 * 4 * kJW * kVld * sizeof(double);
-    static bool wattr = false;
-    if (!wattr) {
-      TR_CUDA(cudaFuncSetAttribute(k_face_svt_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)sm));
-      wattr = true;
-    }
-    launch("face_svt", k_face_svt_warp, (unsigned)cdiv(nfa, 4), 128, sm, st, (double2*)faces,
-           (int)sh.r0, (int)sh.r1, nfa, pen, tau);
   } else {
     // one warp per Jacobi pair: no idle warps at the per-round barrier
     static const int fth_env = getenv("TR_FACE_THREADS") ? atoi(getenv("TR_FACE_THREADS")) : 0;
@@ -718,6 +694,7 @@ __global__ void k_prox(Penalty pen, double mu, const T* __restrict__ v, T* __res
 
 }  // namespace tr
 
+#include "tucker.cuh"
 #include "admm.cuh"
 
 using namespace tr;
@@ -862,6 +839,8 @@ int tr_admm_create(int dtype, int order, const int64_t* dims, int kind, const vo
     TR_REQUIRE(modes[k] >= -1 && modes[k] < order, "gradient mode %lld out of range",
                (long long)modes[k]);
     cfg.modes[k] = (int)modes[k];
+    for (int j = 0; j < k; ++j)
+      TR_REQUIRE(modes[j] != modes[k], "gradient mode %lld repeated", (long long)modes[k]);
   }
   cfg.randomized = randomized;
   for (int i = 0; i < 2; ++i) {
@@ -907,16 +886,54 @@ int tr_admm_read(void* handle, int which, void* dst, void* stream) {
     const void* src = which == 0 ? (const void*)s->lold
                       : which == 1 ? (const void*)s->e
                       : which == 2 ? (const void*)s->y
-                                   : (const void*)s->z;
+                      : which == 3 ? (const void*)s->z
+                                   : (const void*)s->gcur[which - 4];
     const size_t es = sizeof(*s->l);
     TR_CUDA(cudaStreamSynchronize(s->streams[0]));
     TR_CUDA(cudaMemcpyAsync(dst, src, es * s->g.N, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
     (void)sizeof(S);
     return 0;
   };
-  TR_REQUIRE(which >= 0 && which <= 3, "bad state index %d", which);
+  const int nm = h->dtype == TR_F32 ? ((Solver<float>*)h->solver)->cfg.nmodes
+                                     : ((Solver<double>*)h->solver)->cfg.nmodes;
+  TR_REQUIRE(which >= 0 && which < 4 + nm, "bad state index %d", which);
   if (h->dtype == TR_F32) return rd((Solver<float>*)h->solver);
   return rd((Solver<double>*)h->solver);
+}
+
+int tr_admm_set_sketch(void* handle, int sketch_mode, int nproc, const int64_t* proc_order,
+                       const int64_t* ranks, const int64_t* blocks, const int64_t* krylov,
+                       double eps, int64_t block, double defl_tol, uint64_t seed) {
+  TR_REQUIRE(handle && (nproc == 0 || proc_order), "null pointer argument");
+  TR_REQUIRE(sketch_mode == 0 || sketch_mode == 1, "sketch mode must be 0 (fixed-rank) or 1");
+  TR_REQUIRE(nproc >= 0 && nproc <= kTuckerMaxOrder, "too many processed modes");
+  auto* h = (AdmmHandle*)handle;
+  TuckerSpec sp;
+  sp.mode = sketch_mode;
+  sp.nproc = nproc;
+  for (int p = 0; p < nproc; ++p) {
+    sp.proc[p] = (int)proc_order[p];
+    if (sketch_mode == 0) {
+      TR_REQUIRE(ranks && blocks && krylov, "fixed-rank sketching needs ranks, blocks and krylov");
+      sp.ranks[p] = ranks[p];
+      sp.blocks[p] = blocks[p];
+      sp.krylov[p] = krylov[p];
+    }
+  }
+  TR_REQUIRE(sketch_mode == 0 || (eps > 0 && eps < 1 && block >= 1), "bad fixed-accuracy sketch");
+  sp.eps = eps;
+  sp.block = block;
+  sp.defl_tol = defl_tol;
+  sp.seed = seed;
+  auto set = [&](auto* s) -> int {
+    for (int p = 0; p < nproc; ++p)
+      TR_REQUIRE(sp.proc[p] >= 0 && sp.proc[p] < s->order, "processing order entry out of range");
+    s->tspec = sp;
+    s->generic = true;
+    return 0;
+  };
+  if (h->dtype == TR_F32) return set((Solver<float>*)h->solver);
+  return set((Solver<double>*)h->solver);
 }
 
 void* tr_admm_stream(void* handle) {
@@ -932,6 +949,148 @@ int tr_admm_destroy(void* handle) {
   cudaDeviceSynchronize();
   if (h->dtype == TR_F32) delete (Solver<float>*)h->solver;
   else delete (Solver<double>*)h->solver;
+  delete h;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// generic Tucker engine (tucker.cuh)
+// ---------------------------------------------------------------------------
+namespace {
+struct TuckerHandle {
+  int dtype;
+  tr::TuckerResult res;
+};
+}  // namespace
+
+int tr_tucker_create(int dtype, const void* a, int order, const int64_t* dims, int sketch_mode,
+                     int nproc, const int64_t* proc_order, const int64_t* ranks,
+                     const int64_t* blocks, const int64_t* krylov, double eps, int64_t block,
+                     double defl_tol, uint64_t seed, void* stream, void** handle) {
+  TR_REQUIRE(a && dims && handle && (nproc == 0 || proc_order), "null pointer argument");
+  TR_REQUIRE(dtype == TR_F32 || dtype == TR_F64, "dtype must be TR_F32 or TR_F64");
+  TR_REQUIRE(order >= 1 && order <= kTuckerMaxOrder, "order must be in [1, %d]", kTuckerMaxOrder);
+  TR_REQUIRE(sketch_mode == 0 || sketch_mode == 1, "sketch mode must be 0 (fixed-rank) or 1");
+  TR_REQUIRE(nproc >= 0 && nproc <= kTuckerMaxOrder, "too many processed modes");
+  for (int i = 0; i < order; ++i) TR_REQUIRE(dims[i] >= 1, "empty tensors are not supported");
+  TuckerSpec sp;
+  sp.mode = sketch_mode;
+  sp.nproc = nproc;
+  for (int p = 0; p < nproc; ++p) {
+    TR_REQUIRE(proc_order[p] >= 0 && proc_order[p] < order, "processing order entry %lld out of range",
+               (long long)proc_order[p]);
+    sp.proc[p] = (int)proc_order[p];
+    if (sketch_mode == 0) {
+      TR_REQUIRE(ranks && blocks && krylov, "fixed-rank sketching needs ranks, blocks and krylov");
+      sp.ranks[p] = ranks[p];
+      sp.blocks[p] = blocks[p];
+      sp.krylov[p] = krylov[p];
+      TR_REQUIRE(ranks[p] >= 1 && ranks[p] <= dims[proc_order[p]], "rank %lld out of range for mode %lld",
+                 (long long)ranks[p], (long long)proc_order[p]);
+      TR_REQUIRE(blocks[p] >= 1 && blocks[p] <= ranks[p], "block size must satisfy 1 <= b <= r");
+      TR_REQUIRE((krylov[p] + 1) * blocks[p] >= ranks[p], "(q+1)*b < rank");
+    }
+  }
+  if (sketch_mode == 1) {
+    TR_REQUIRE(eps > 0 && eps < 1, "eps must lie in (0, 1)");
+    TR_REQUIRE(block >= 1, "block size must be >= 1");
+  }
+  sp.eps = eps;
+  sp.block = block;
+  sp.defl_tol = defl_tol;
+  sp.seed = seed;
+  auto* h = new TuckerHandle{dtype, {}};
+  cudaStream_t st = (cudaStream_t)stream;
+  const int rc = dtype == TR_F32
+                     ? tucker_compress<float>((const float*)a, order, dims, sp, h->res, st)
+                     : tucker_compress<double>((const double*)a, order, dims, sp, h->res, st);
+  if (rc) {
+    delete h;
+    return rc;
+  }
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    delete h;
+    TR_CUDA(e);
+  }
+  *handle = h;
+  return 0;
+}
+
+int tr_tucker_info(void* handle, int64_t* core_dims, int64_t* ranks, int64_t* processed,
+                   double* energy, int64_t* deflations, int64_t* iterations, double* orth_loss) {
+  TR_REQUIRE(handle, "null handle");
+  const TuckerResult& r = ((TuckerHandle*)handle)->res;
+  for (int i = 0; i < r.order; ++i) {
+    if (core_dims) core_dims[i] = r.cdims[i];
+    if (ranks) ranks[i] = r.processed[i] ? r.ranks[i] : r.dims[i];
+    if (processed) processed[i] = r.processed[i] ? 1 : 0;
+    if (energy) energy[i] = r.energy[i];
+    if (deflations) deflations[i] = r.deflations[i];
+    if (iterations) iterations[i] = r.iterations[i];
+    if (orth_loss) orth_loss[i] = r.orth_loss[i];
+  }
+  return 0;
+}
+
+int tr_tucker_read(void* handle, int which, double* dst, void* stream) {
+  TR_REQUIRE(handle && dst, "null pointer argument");
+  const TuckerResult& r = ((TuckerHandle*)handle)->res;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (which < 0) {
+    const int64_t n = r.core_size();
+    if (n > 0 && r.core) TR_CUDA(cudaMemcpyAsync(dst, r.core, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    return 0;
+  }
+  TR_REQUIRE(which < r.order && r.processed[which], "mode %d was not processed", which);
+  const int64_t n = r.dims[which] * r.ranks[which];
+  if (n > 0 && r.factors[which])
+    TR_CUDA(cudaMemcpyAsync(dst, r.factors[which], sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  return 0;
+}
+
+int tr_tucker_svt(void* handle, int transform_kind, const void* transform_mats,
+                  const double* alphas, int penalty_kind, double p0, double p1, double tau,
+                  void* out, void* stream) {
+  TR_REQUIRE(handle && out, "null pointer argument");
+  TR_REQUIRE(transform_kind >= 0 && transform_kind <= 2, "bad transform kind %d", transform_kind);
+  TR_REQUIRE(transform_kind != TR_TRANSFORM_EXPLICIT || (transform_mats && alphas),
+             "explicit transform needs matrices and alphas");
+  TR_REQUIRE(penalty_kind >= 0 && penalty_kind <= 6, "bad penalty kind %d", penalty_kind);
+  TR_REQUIRE(tau >= 0.0, "tau must be >= 0");
+  auto* h = (TuckerHandle*)handle;
+  const TuckerResult& r = h->res;
+  TR_REQUIRE(r.order >= 3, "tensor order %d < required 3", r.order);
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t N = 1;
+  for (int i = 0; i < r.order; ++i) N *= r.dims[i];
+  const size_t es = h->dtype == TR_F32 ? 4 : 8;
+  const int64_t nc = r.core_size();
+  if (nc == 0) {  // rank-0 structure: zeros (sketch.py:453-454)
+    TR_CUDA(cudaMemsetAsync(out, 0, es * N, st));
+    return 0;
+  }
+  double* work = nullptr;
+  TR_CUDA(cudaMallocAsync((void**)&work, sizeof(double) * nc, st));
+  int rc = 0;
+  if (cudaMemcpyAsync(work, r.core, sizeof(double) * nc, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    rc = 2;
+  Penalty pen{penalty_kind, p0, p1};
+  if (!rc)
+    rc = h->dtype == TR_F32
+             ? tucker_core_svt<float>(r, work, transform_kind, transform_mats, alphas, pen, tau, st)
+             : tucker_core_svt<double>(r, work, transform_kind, transform_mats, alphas, pen, tau, st);
+  if (!rc)
+    rc = h->dtype == TR_F32 ? tucker_reconstruct<float>(r, work, (float*)out, st)
+                            : tucker_reconstruct<double>(r, work, (double*)out, st);
+  cudaFreeAsync(work, st);
+  return rc;
+}
+
+int tr_tucker_destroy(void* handle) {
+  if (!handle) return 0;
+  auto* h = (TuckerHandle*)handle;
+  cudaStreamSynchronize(h->res.st);
   delete h;
   return 0;
 }
@@ -1073,12 +1232,3 @@ int tr_profile_read(char* names, int64_t names_len, double* ms, int64_t* counts,
 }
 
 }  // extern "C"
-
-extern "C" int tr_debug_read(int* out, int reset) {
-  cudaDeviceSynchronize();
-  for (int i = 0; i < 8; ++i) {
-    out[i] = tr::g_dbg[i];
-    if (reset) tr::g_dbg[i] = 0;
-  }
-  return 0;
-}

@@ -330,7 +330,10 @@ __device__ __forceinline__ void jacobi_cs(double app, double aqq, double apq, do
 // absorb.  Shortens the serial latency chain of a Jacobi round.
 __device__ __forceinline__ void jacobi_cs_fast(double app, double aqq, double apq, double& c,
                                                double& s) {
-  const double r = (aqq - app) * 0.5 * fast_rcp(apq);
+  // fast_rcp starts from an fp32 reciprocal: outside [1e-30, 1e30] use the
+  // IEEE division (a tiny or huge a_pq would give inf / 0 there)
+  const double ra = fabs(apq);
+  const double r = (aqq - app) * 0.5 * ((ra > 1e-30 && ra < 1e30) ? fast_rcp(apq) : 1.0 / apq);
   const float rf = (float)r;
   float tf;
   if (fabsf(rf) > 1e15f) tf = 0.5f / rf;
@@ -586,7 +589,6 @@ __global__ void __launch_bounds__(256) k_ritz(const double* __restrict__ Mfull, 
       __syncthreads();
       if (threadIdx.x == 0) rot_any = 0;
       __syncthreads();
-      if (threadIdx.x == 0) atomicAdd(&g_dbg[0], 1);  // ritz sweeps
       if (!any) break;
     }
   } else {
@@ -662,7 +664,6 @@ __global__ void __launch_bounds__(256) k_ritz(const double* __restrict__ Mfull, 
       __syncthreads();
       if (threadIdx.x == 0) rot_any = 0;
       __syncthreads();
-      if (threadIdx.x == 0) atomicAdd(&g_dbg[0], 1);  // ritz sweeps
       if (!any) break;
     }
   }

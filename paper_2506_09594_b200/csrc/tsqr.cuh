@@ -109,9 +109,16 @@ __global__ void __launch_bounds__(1024) k_tsqr_local(const double* __restrict__ 
 // Stage 2 (one CTA): QR of the stack, pivoted QR of its s x s R with the
 // reference's deflation rule, and C = Q_top [Q_piv[:, :s_eff]; 0] (zero
 // columns beyond s_eff).  info[0] <- s_eff.
+//   tol_abs > 0   absolute deflation tolerance (defl_qr(a, tol), sketch.py:146-164)
+//   tol_abs == 0  1e-14 ||K||_F (the Krylov basis rule, sketch.py:179)
+//   tol_abs < 0   no deflation (every column kept)
+//   pivot == 0    plain Householder QR (np.linalg.qr) instead of geqp3 pivoting
+//   Rout          optional s x s: rows < s_eff hold R with the pivoting undone
+//                 (r_out[:, piv] = r[:s_eff, :]), rows >= s_eff zero
 __global__ void __launch_bounds__(1024) k_tsqr_top(const double* __restrict__ Rstack, int nrows,
                                                   int s, double* __restrict__ Cout,
-                                                  int64_t* __restrict__ info) {
+                                                  int64_t* __restrict__ info, double tol_abs,
+                                                  int pivot, double* __restrict__ Rout) {
   extern __shared__ double tsqr_smem[];
   const int ld = nrows + 1;
   double* S = tsqr_smem;                       // nrows x s stack -> reflectors
@@ -138,7 +145,8 @@ __global__ void __launch_bounds__(1024) k_tsqr_top(const double* __restrict__ Rs
     const int i = e % s, j = e / s;
     if (i <= j) f2 += S[i + ld * j] * S[i + ld * j];
   }
-  const double tol = 1e-14 * sqrt(block_sum(f2, red));
+  const double fro = sqrt(block_sum(f2, red));
+  const double tol = tol_abs > 0.0 ? tol_abs : tol_abs == 0.0 ? 1e-14 * fro : -1.0;
   for (int e = threadIdx.x; e < s * s; e += blockDim.x) {
     const int i = e % s, j = e / s;
     Rp[i + lrp * j] = i <= j ? S[i + ld * j] : 0.0;
@@ -157,14 +165,18 @@ __global__ void __launch_bounds__(1024) k_tsqr_top(const double* __restrict__ Rs
     __syncthreads();
     if (threadIdx.x == 0) {
       int best = k;
-      for (int j = k + 1; j < s; ++j)
-        if (cn[j] > cn[best]) best = j;
+      if (pivot)
+        for (int j = k + 1; j < s; ++j)
+          if (cn[j] > cn[best]) best = j;
       const double nb = sqrt(cn[best]);
-      if (!(nb >= tol) || nb == 0.0) s_eff_s = k;
+      if (tol >= 0.0 && (!(nb >= tol) || nb == 0.0)) {
+        s_eff_s = k;
+      } else {
+        const int t = perm[k];
+        perm[k] = perm[best];
+        perm[best] = t;
+      }
       best_s = best;
-      const int t = perm[k];
-      perm[k] = perm[best];
-      perm[best] = t;
     }
     __syncthreads();
     if (s_eff_s == k) break;
@@ -209,6 +221,11 @@ __global__ void __launch_bounds__(1024) k_tsqr_top(const double* __restrict__ Rs
     __syncthreads();
   }
   const int se = s_eff_s;
+  if (Rout)
+    for (int e = threadIdx.x; e < s * s; e += blockDim.x) {
+      const int i = e % s, j = e / s;
+      Rout[i + (int64_t)s * perm[j]] = (i < se && i <= j) ? Rp[i + lrp * j] : 0.0;
+    }
   // C = [Q_piv[:, :se]; 0] (columns >= se zero), then C <- Q_top C
   for (int e = threadIdx.x; e < nrows * s; e += blockDim.x) {
     const int i = e % nrows, j = e / nrows;
@@ -250,7 +267,7 @@ __global__ void __launch_bounds__(1024) k_tsqr_form(const double* __restrict__ V
     const int i = e % rows, j = e / rows;
     const double z = Zs[i + ld * j];
     Z[r0 + i + m * j] = z;
-    Zt[r0 + i + m * j] = (T)z;
+    if (Zt) Zt[r0 + i + m * j] = (T)z;
   }
 }
 

@@ -1,15 +1,23 @@
 """Randomized Tucker sketching and the randomized t-SVT on the B200.
 
-Drop-in for tenrec/sketch.py's fixed-rank path:
+Drop-in for tenrec/sketch.py:
   SketchConfig          sketch.py:64-126 (same fields, defaults and errors)
   TuckerFactors         sketch.py:39-61
-  rsthosvd_bki          sketch.py:211-270  -> C ABI tr_rsthosvd_bki
-  gnhtsvt_randomized    sketch.py:430-456  -> C ABI tr_gnhtsvt_randomized
+  BLBPDiagnostics       sketch.py:129-143
+  rsthosvd_bki          sketch.py:211-270  -> C ABI tr_rsthosvd_bki (order (0, 1))
+                                              or the generic engine tr_tucker_*
+  ad_rsthosvd_blbp      sketch.py:355-403  -> tr_tucker_* (block Lanczos)
+  gnhtsvt_randomized    sketch.py:430-456  -> tr_gnhtsvt_randomized (fixed-rank,
+                                              order (0, 1): the ADMM hot path)
+                                              or tr_tucker_create + tr_tucker_svt
 
 Sketch matrices come from the counter-based Philox stream (entry (c, t) of
 processing step p is N(0,1) at (seed, p, c*b + t)), so results are
 deterministic per seed and identical to the oracle fed the same stream.
-``sketch_override=(g0, g1)`` replays externally drawn matrices instead.
+``sketch_override=(g0, g1)`` replays externally drawn matrices instead.  The
+block Lanczos path numbers its Gaussian draws in call order across all modes:
+draw j (the start block of a mode or a fill block) is the (n, cols) matrix of
+entries N(0,1) at (seed, j, c*cols + t).
 """
 
 from __future__ import annotations
@@ -110,11 +118,127 @@ class SketchConfig:
         return vals
 
 
-def _gpu_order_check(order):
-    if tuple(order) != (0, 1):
-        raise NotImplementedError(
-            f"the B200 path compresses modes (0, 1) (the gnhtsvt_randomized default); "
-            f"order {tuple(order)} is not supported yet")
+@dataclass
+class BLBPDiagnostics:
+    """Per-mode traces of the fixed-accuracy sweep (sketch.py:129-143)."""
+
+    energy_estimates: dict = field(default_factory=dict)
+    ranks: dict = field(default_factory=dict)
+    deflations: dict = field(default_factory=dict)
+    orth_loss: dict = field(default_factory=dict)
+    iterations: dict = field(default_factory=dict)
+
+    @property
+    def implied_error(self) -> float:
+        total = sum(max(e, 0.0) for e in self.energy_estimates.values())
+        return float(np.sqrt(total))
+
+
+class TuckerRun:
+    """One compression by the generic device engine (C ABI tr_tucker_*):
+    factors, core and diagnostics stay on the device until read."""
+
+    def __init__(self, cm: ColMajor, sketch: SketchConfig, order, stream=None):
+        self.lib = _lib.lib()
+        self.cm = cm
+        self.dims = cm.dims
+        d = len(self.dims)
+        order = tuple(int(k) for k in order)
+        if sketch.mode == "fixed-rank":
+            ranks, blocks, krylov = sketch.resolved_fixed_rank(order)
+            mode = 0
+        else:
+            ranks = blocks = krylov = [0] * len(order)
+            mode = 1
+        handle = ctypes.c_void_p()
+        _lib.check(self.lib.tr_tucker_create(
+            cm.dtype_code, ctypes.c_void_p(cm.ptr), d, _lib.i64(self.dims), mode, len(order),
+            _lib.i64(order), _lib.i64(ranks), _lib.i64(blocks), _lib.i64(krylov),
+            float(sketch.eps), int(sketch.block),
+            float(sketch.defl_tol) if sketch.defl_tol is not None else 0.0,
+            ctypes.c_uint64(int(sketch.seed) & (2 ** 64 - 1)), _lib.stream_ptr(stream),
+            ctypes.byref(handle)))
+        self.handle = handle
+        cdims = (ctypes.c_int64 * d)()
+        rks = (ctypes.c_int64 * d)()
+        proc = (ctypes.c_int64 * d)()
+        en = (ctypes.c_double * d)()
+        dfl = (ctypes.c_int64 * d)()
+        its = (ctypes.c_int64 * d)()
+        orl = (ctypes.c_double * d)()
+        _lib.check(self.lib.tr_tucker_info(handle, cdims, rks, proc, en, dfl, its, orl))
+        self.core_dims = tuple(int(v) for v in cdims)
+        self.ranks = tuple(int(v) for v in rks)
+        self.processed = tuple(bool(v) for v in proc)
+        self.order = order
+        self.diag = BLBPDiagnostics()
+        for k in order:
+            self.diag.energy_estimates[k] = float(en[k])
+            self.diag.ranks[k] = int(rks[k])
+            self.diag.deflations[k] = int(dfl[k])
+            self.diag.iterations[k] = int(its[k])
+            self.diag.orth_loss[k] = float(orl[k])
+
+    def factors(self):
+        import torch
+
+        out = []
+        for k, n in enumerate(self.dims):
+            if not self.processed[k]:
+                out.append(None)
+                continue
+            r = self.ranks[k]
+            f = torch.empty(max(n * r, 1), dtype=torch.float64, device="cuda")
+            if r:
+                _lib.check(self.lib.tr_tucker_read(self.handle, k, ctypes.c_void_p(f.data_ptr()),
+                                                   _lib.stream_ptr()))
+            out.append(f[:n * r].reshape(r, n).T)
+        return out
+
+    def core(self):
+        import torch
+
+        nc = int(math.prod(self.core_dims))
+        c = torch.empty(max(nc, 1), dtype=torch.float64, device="cuda")
+        if nc:
+            _lib.check(self.lib.tr_tucker_read(self.handle, -1, ctypes.c_void_p(c.data_ptr()),
+                                               _lib.stream_ptr()))
+        d = len(self.core_dims)
+        return c[:nc].reshape(tuple(reversed(self.core_dims))).permute(*reversed(range(d)))
+
+    def svt(self, transform, penalty, tau, out: ColMajor, stream=None):
+        kind, p0, p1 = encode_penalty(penalty)
+        tcode, tmats, talphas, keep = transform.device_args(self.core_dims) \
+            if transform.kind == "explicit" else transform.device_args(self.dims)
+        _lib.check(self.lib.tr_tucker_svt(self.handle, tcode, tmats, talphas, kind, p0, p1,
+                                          float(tau), ctypes.c_void_p(out.ptr),
+                                          _lib.stream_ptr(stream)))
+        del keep
+
+    def tucker_factors(self, as_numpy: bool):
+        factors = self.factors()
+        core = self.core()
+        if as_numpy:
+            factors = [f.cpu().numpy() if f is not None else None for f in factors]
+            core = core.cpu().numpy()
+        return TuckerFactors(core=core, factors=factors, dims=tuple(self.dims))
+
+    def close(self):
+        if self.handle:
+            self.lib.tr_tucker_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _fast_path(sketch: SketchConfig, order) -> bool:
+    """The asynchronous fused launch sequence (lrta.cu) handles fixed-rank
+    compression of modes (0, 1) -- the ADMM hot path; the generic engine the rest."""
+    return sketch.mode == "fixed-rank" and tuple(order) == (0, 1)
 
 
 def _override_ptrs(override, cm: ColMajor):
@@ -132,15 +256,21 @@ def _override_ptrs(override, cm: ColMajor):
     return ptrs[0], ptrs[1], keep
 
 
+def _with_default_order(sketch: SketchConfig) -> SketchConfig:
+    """gnhtsvt_randomized's default: compress modes 0 and 1 only (sketch.py:444-451)."""
+    if sketch.order is not None:
+        return sketch
+    return SketchConfig(mode=sketch.mode, order=(0, 1), ranks=sketch.ranks,
+                        blocks=sketch.blocks, krylov=sketch.krylov, eps=sketch.eps,
+                        block=sketch.block, defl_tol=sketch.defl_tol, seed=sketch.seed)
+
+
 def _resolve(sketch: SketchConfig, dims):
-    if sketch.order is None:
-        sketch = SketchConfig(mode=sketch.mode, order=(0, 1), ranks=sketch.ranks,
-                              blocks=sketch.blocks, krylov=sketch.krylov, eps=sketch.eps,
-                              block=sketch.block, defl_tol=sketch.defl_tol, seed=sketch.seed)
+    """(sketch, ranks, blocks, krylov) of the fused fixed-rank (0, 1) path."""
+    sketch = _with_default_order(sketch)
     sketch.validate(dims)
-    if sketch.mode != "fixed-rank":
-        raise NotImplementedError("fixed-accuracy (BLBP) sketching is not on the B200 path yet")
-    _gpu_order_check(sketch.order)
+    if not _fast_path(sketch, sketch.order):
+        raise ValueError("the fused path compresses modes (0, 1) with a fixed-rank sketch")
     ranks, blocks, krylov = sketch.resolved_fixed_rank(sketch.order)
     return sketch, ranks, blocks, krylov
 
@@ -165,11 +295,24 @@ def gnhtsvt_randomized(a, transform=DEFAULT_TRANSFORM, penalty=None, tau: float 
         raise ValueError(f"tensor order {len(dims)} < required 3")
     if any(n <= 0 for n in dims):
         raise ValueError(f"empty tensors are not supported, got shape {dims}")
-    transform.check_shape(dims)
-    sketch, ranks, blocks, krylov = _resolve(sketch, dims)
+    sketch = _with_default_order(sketch)
+    sketch.validate(dims)
     out = empty_like(cm)
-    _run_lrta(cm, out, ranks, blocks, krylov, sketch.seed, transform, penalty, tau,
-              sketch_override)
+    if _fast_path(sketch, sketch.order):
+        transform.check_shape(dims)
+        ranks, blocks, krylov = sketch.resolved_fixed_rank(sketch.order)
+        _run_lrta(cm, out, ranks, blocks, krylov, sketch.seed, transform, penalty, tau,
+                  sketch_override)
+    else:
+        if sketch_override is not None:
+            raise ValueError("sketch_override applies to the fixed-rank (0, 1) path only")
+        run = TuckerRun(cm, sketch, sketch.order)
+        try:
+            if transform.kind == "explicit":
+                transform.check_shape(run.core_dims)
+            run.svt(transform, penalty, tau, out)
+        finally:
+            run.close()
     return out if isinstance(a, ColMajor) else from_device(out)
 
 
@@ -196,27 +339,43 @@ def _run_lrta(cm, out, ranks, blocks, krylov, seed, transform, penalty, tau, ske
 
 def rsthosvd_bki(x, ranks, order=None, blocks=None, krylov=None, seed: int = 0,
                  strict_rank: bool = True, sketch_override=None):
-    """Fixed-rank randomized Tucker compression of modes (0, 1) on the GPU.
+    """Fixed-rank randomized Tucker compression on the GPU (sketch.py:211-270).
 
-    Factor columns carry the canonical sign (largest-|entry| positive).  With
-    ``strict_rank`` a Krylov block that deflates below a target rank raises,
-    like the reference.
+    ``order`` defaults to every mode, like the reference.  Factor columns
+    carry the canonical sign (largest-|entry| positive).  With ``strict_rank``
+    a Krylov block that deflates below a target rank raises, like the
+    reference; an all-zero input gives a rank-0 structure.
     """
     import torch
 
     cm = x if isinstance(x, ColMajor) else to_device(x)
     dims = cm.dims
-    order = (0, 1) if order is None else tuple(order)
+    order = tuple(range(len(dims))) if order is None else tuple(int(k) for k in order)
     cfg = SketchConfig(mode="fixed-rank", order=order, ranks=tuple(ranks),
                        blocks=tuple(blocks) if blocks else None,
                        krylov=tuple(krylov) if krylov is not None else None, seed=seed)
     cfg.validate(dims)
-    _gpu_order_check(order)
     rks, bls, krs = cfg.resolved_fixed_rank(order)
+    if order != (0, 1) or len(dims) < 3 or not bool(cm.flat.any()):
+        if sketch_override is not None:
+            raise ValueError("sketch_override applies to the order (0, 1) path only")
+        run = TuckerRun(cm, cfg, order)
+        try:
+            for k, r in zip(order, rks):
+                if run.ranks[k] == 0:
+                    break  # a zero unfolding: rank-0 structure, no rank check (sketch.py:246-252)
+                if strict_rank and run.ranks[k] < r:
+                    raise ValueError(f"Krylov block numerically rank deficient on mode {k}: "
+                                     f"rank {run.ranks[k]} < target {r}")
+            return run.tucker_factors(cm.kind == "numpy")
+        finally:
+            run.close()
     lib = _lib.lib()
     d = _lib.i64(dims)
     rk, bl, kr = _lib.i64(rks), _lib.i64(bls), _lib.i64(krs)
     nbytes = lib.tr_lrta_workspace(cm.dtype_code, len(dims), d, rk, bl, kr)
+    if nbytes < 0:
+        _lib.check(1)
     ws = workspace(nbytes)
     nf = int(math.prod(dims[2:]))
     f0 = torch.empty(dims[0] * rks[0], dtype=torch.float64, device="cuda")
@@ -244,3 +403,20 @@ def rsthosvd_bki(x, ranks, order=None, blocks=None, krylov=None, seed: int = 0,
         factors = [f.cpu().numpy() if f is not None else None for f in factors]
         C = C.cpu().numpy()
     return TuckerFactors(core=C, factors=factors, dims=tuple(dims))
+
+
+def ad_rsthosvd_blbp(x, eps: float, block: int = 10, defl_tol: float = None, order=None,
+                     seed: int = 0):
+    """Fixed-accuracy Tucker compression by block Lanczos bidiagonalisation
+    (sketch.py:355-403) on the GPU.  Returns ``(TuckerFactors, BLBPDiagnostics)``."""
+    cm = x if isinstance(x, ColMajor) else to_device(x)
+    dims = cm.dims
+    order = tuple(range(len(dims))) if order is None else tuple(int(k) for k in order)
+    cfg = SketchConfig(mode="fixed-accuracy", order=order, eps=eps, block=block,
+                       defl_tol=defl_tol, seed=seed)
+    cfg.validate(dims)
+    run = TuckerRun(cm, cfg, order)
+    try:
+        return run.tucker_factors(cm.kind == "numpy"), run.diag
+    finally:
+        run.close()

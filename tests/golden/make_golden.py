@@ -179,6 +179,71 @@ def main():
     out["obr_res"] = np.array(rep.residual_history)
     del onebit, solvers
 
+    # -- fixed-accuracy block Lanczos (ad_rsthosvd_blbp) and other orders ------
+    # (a separate generator: the cases above stay bit-identical)
+    rng2 = np.random.default_rng(2468)
+    bcases = [
+        # dims, lowrank (0 = none), noise, eps, block, defl_tol, order, seed
+        ((14, 12, 6), 3, 1e-3, 0.1, 3, None, None, 5),
+        ((16, 18, 5), 4, 0.0, 0.05, 4, None, (1, 0), 9),
+        ((12, 10, 4, 3), 0, 0.0, 0.3, 5, None, (0, 1), 2),
+        ((20, 8, 6), 2, 1e-2, 0.02, 3, 1e-6, (0, 2, 1), 13),
+        ((40, 30, 6), 0, 0.0, 0.2, 4, None, (0, 1), 21),
+    ]
+    for i, (dims, lr, noise, eps, block, dtol, order, seed) in enumerate(bcases):
+        if lr:
+            core = rng2.standard_normal((lr,) * len(dims))
+            a = core
+            for k, n in enumerate(dims):
+                a = tenrec.mode_product(a, rng2.standard_normal((n, lr)), k)
+            a = a + noise * rng2.standard_normal(dims)
+        else:
+            a = rng2.standard_normal(dims)
+        tf, diag = tenrec.ad_rsthosvd_blbp(a, eps, block=block, defl_tol=dtol, order=order,
+                                           seed=seed)
+        pre = f"blbp{i}_"
+        out[pre + "in"] = a
+        out[pre + "eps"] = np.array(eps)
+        out[pre + "block"] = np.array(block)
+        out[pre + "defl_tol"] = np.array(-1.0 if dtol is None else dtol)
+        out[pre + "order"] = np.array(order if order is not None else tuple(range(len(dims))))
+        out[pre + "seed"] = np.array(seed)
+        out[pre + "core"] = tf.core
+        for k, f in enumerate(tf.factors):
+            if f is not None:
+                out[pre + f"f{k}"] = f
+        for name in ("energy_estimates", "ranks", "deflations", "orth_loss", "iterations"):
+            d = getattr(diag, name)
+            out[pre + name] = np.array([d[k] for k in sorted(d)], dtype=np.float64)
+        sk = tenrec.SketchConfig(mode="fixed-accuracy", order=order, eps=eps, block=block,
+                                 defl_tol=dtol, seed=seed)
+        if len(dims) >= 3:
+            out[pre + "svt"] = tenrec.gnhtsvt_randomized(a, tenrec.Transform.fft(), pens["mcp"],
+                                                         0.3, sk)
+    # fixed-rank compression of every mode / other orders (reference PCG64 draws)
+    ocases = [((12, 11, 7), (4, 4, 3), None, None, 3),
+              ((10, 12, 6), (5, 4), (1, 0), (2, 2), 8),
+              ((9, 10, 8, 3), (4, 3, 3), (2, 0, 1), (3, 2, 1), 4)]
+    for i, (dims, ranks, order, blocks, seed) in enumerate(ocases):
+        a = rng2.standard_normal(dims)
+        tf = tenrec.rsthosvd_bki(a, ranks, order=order, blocks=blocks, krylov=None, seed=seed,
+                                 strict_rank=False)
+        pre = f"ord{i}_"
+        out[pre + "in"] = a
+        out[pre + "ranks"] = np.array(ranks)
+        out[pre + "order"] = np.array(order if order is not None else tuple(range(len(dims))))
+        out[pre + "blocks"] = np.array(blocks if blocks is not None
+                                       else tuple(max(1, int(np.ceil(r / 4))) for r in ranks))
+        out[pre + "seed"] = np.array(seed)
+        out[pre + "core"] = tf.core
+        for k, f in enumerate(tf.factors):
+            if f is not None:
+                out[pre + f"f{k}"] = f
+        sk = tenrec.SketchConfig(mode="fixed-rank", order=order or tuple(range(len(dims))),
+                                 ranks=ranks, blocks=blocks, seed=seed)
+        out[pre + "svt"] = tenrec.gnhtsvt_randomized(a, tenrec.Transform.fft(), pens["mcp"], 0.3,
+                                                     sk)
+
     path = os.path.join(HERE, "reference_vectors.npz")
     np.savez_compressed(path, **out)
     print(f"wrote {path}: {len(out)} arrays, {os.path.getsize(path)} bytes")

@@ -88,15 +88,16 @@ def _lowrank_problem(seed=5):
     return np.where(mask, x, 0.0), mask
 
 
-@pytest.mark.parametrize("ranks,fp32_tol", [((4, 4), 1e-4), ((8, 8), 1e-3)])
-def test_larger_randomized_power_of_two(cuda_lib, ranks, fp32_tol):
+@pytest.mark.parametrize("ranks", [(4, 4), (8, 8)])
+def test_larger_randomized_power_of_two(cuda_lib, ranks):
     """64 x 64 x 16: radix-2 FFT passes, fused panels, tcgen05 projection.
 
-    ranks (4, 4) = the signal's multilinear rank (well posed).  ranks (8, 8)
-    makes Ritz vectors 5-8 span a near-null space: even the fp64 path drifts
-    from 1e-16 to 1e-12 there, and fp32 reaches ~2e-4 after 6 sweeps; that
-    case documents the drift bound rather than the 1e-4 parity target.
+    ranks (4, 4) = the signal's multilinear rank; ranks (8, 8) makes Ritz
+    vectors 5-8 span a near-null space.  Both meet the 1e-4 fp32 bar after 6
+    sweeps (tools/f32_drift_probe.py: 2.2e-5 and 3.4e-5 on the B200; the
+    CUDA-core fallback panels, TR_NO_PANEL, drift to 4.5e-4 on (8, 8)).
     """
+    fp32_tol = 1e-4
     import paper_2506_09594_b200 as pk
     mobs, mask = _lowrank_problem()
     sk = pk.SketchConfig(mode="fixed-rank", order=(0, 1), ranks=ranks, blocks=(2, 2),
