@@ -324,13 +324,25 @@ static int bki_generic(const T* A, int64_t m, int64_t n, int64_t inner, int r, i
 
 // ---- one mode: block Lanczos bidiagonalisation -----------------------------------
 
-// partial sums of A V (m x b, fp64) with the rows of V (T, row-major n x b) fed
-// to the sketch pass as an override (panel kernels; CUDA-core fallback)
+// W (m x b, fp64) = A V for V (n x b, fp64, column-major): fp64-accumulated
+// partial sums over column splits, reduced in a fixed order
 template <typename T>
-static int64_t bki_pass(const T* A, int64_t m, int64_t n, int b, const T* rows, SketchSpec sk,
-                        Bufs<T>& bf, cudaStream_t st) {
-  if (panel_ok<T>(A, m, b)) return panel<T, 0>(A, m, n, b, nullptr, rows, sk, bf.coef, bf.partial, st);
-  return rank_update<T>(A, m, n, b, nullptr, rows, sk, bf.partial, st);
+static void av_pass(const T* A, int64_t m, int64_t n, int b, const double* V, double* partial,
+                    int64_t max_parts, double* W, cudaStream_t st) {
+  const int64_t rowtiles = cdiv(m, 256);
+  int64_t splits = std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 4 * num_sms() / rowtiles));
+  splits = std::min(splits, max_parts);
+  const int64_t cps = cdiv(n, splits);
+  const int64_t sp = cdiv(n, cps);
+  dim3 grid((unsigned)rowtiles, (unsigned)sp);
+  if (b <= 8)
+    launch("tucker", k_av_partial<T, 8>, grid, 256, 0, st, A, m, n, b, V, cps, partial);
+  else if (b <= 16)
+    launch("tucker", k_av_partial<T, 16>, grid, 256, 0, st, A, m, n, b, V, cps, partial);
+  else
+    launch("tucker", k_av_partial<T, 32>, grid, 256, 0, st, A, m, n, b, V, cps, partial);
+  launch("reduce_partials", k_reduce_partials, (unsigned)cdiv(m * b, 32), 256, 0, st,
+         (const double*)partial, (int)sp, m * b, W);
 }
 
 static double host_spectral_norm(const std::vector<double>& a, int rows, int cols);
@@ -375,22 +387,16 @@ static int blbp_generic(const T* A, int64_t m, int64_t n, int64_t inner, double 
   double* Cproj = tmp.get<double>(vmax * b);
   const int64_t max_part = std::max<int64_t>(vmax * b * 64, 1 << 16);
   double* tpart = tmp.get<double>(max_part);
-  T* Vrows = tmp.get<T>((n + 16) * b);
-  T* Ut = tmp.get<T>(m * b);
-  T* Wt = tmp.get<T>(n * b);
+  double* Rt = tmp.get<double>(b * b);
+  const int64_t av_parts = 4ll * num_sms();
+  double* avpart = tmp.get<double>(av_parts * m * b);
   int64_t* info = tmp.get<int64_t>(8);
-  // the block Krylov buffers serve the A v passes (panel kernels + partials)
-  Carve sz(nullptr);
-  Bufs<T> bf;
-  carve_mode<T>(sz, m, n, b, b, 1, bf);
-  char* ws = tmp.get<char>(sz.off);
   Tsqr qm, qn;
-  TR_REQUIRE(ws && !tmp.failed && !ar.failed, "device allocation failed (out of memory?)");
-  Carve cv(ws);
-  carve_mode<T>(cv, m, n, b, b, 1, bf);
+  TR_REQUIRE(!tmp.failed && !ar.failed, "device allocation failed (out of memory?)");
   TR_REQUIRE(tsqr_plan_levels(m, b, tmp, qm) && tsqr_plan_levels(n, b, tmp, qn),
              "QR workspace allocation failed");
-  SketchSpec sk{seed, 0, n, nullptr, 0};  // inner = n: rows read as given (gover)
+  const unsigned pgrid =
+      (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n * 32, 256), 16ll * num_sms()));
 
   // r = (Q, R, s_eff) of an m x bc or n x bc block
   auto qr = [&](Tsqr& q, const double* X, int64_t rows, int bc, double t, int piv, double* Q,
@@ -424,10 +430,7 @@ static int blbp_generic(const T* A, int64_t m, int64_t n, int64_t inner, double 
   while (iters < max_iters) {
     ++iters;
     // w = A v_cur (- u_prev l_prev)            sketch.py:317-320
-    launch("tucker", k_rows_of<T>, grid_cap(n * bc), 256, 0, st, (const double*)Vcur, n, bc, Vrows);
-    const int64_t np = bki_pass<T>(A, m, n, bc, Vrows, sk, bf, st);
-    launch("reduce_partials", k_reduce_partials, (unsigned)cdiv(m * bc, 32), 256, 0, st,
-           (const double*)bf.partial, (int)np, m * bc, W);
+    av_pass<T>(A, m, n, bc, Vcur, avpart, av_parts, W, st);
     if (su_prev > 0)
       tall_small<double>(U + m * (ku - su_prev), m, m, (int)su_prev, Lprev, b, bc, -1.0, 1.0, W, m,
                          st);
@@ -451,11 +454,10 @@ static int blbp_generic(const T* A, int64_t m, int64_t n, int64_t inner, double 
     int64_t sv = 0;
     int cols_next = 0;
     if (su > 0) {
-      launch("tucker", k_convert<double, T>, grid_cap(m * su), 256, 0, st, (const double*)Qm, Ut,
-             m * su);
-      dot_cols<T>(A, m, n, Ut, (int)su, Wt, st);
-      launch("tucker", k_w2_form<T>, grid_cap(n), 256, 0, st, (const T*)Wt, n, (int)su,
-             (const double*)Vcur, bc, (const double*)Rm, b, W2);
+      launch("tucker", k_project_rows<T>, pgrid, 256, 0, st, A, m, n, (const double*)Qm, (int)su,
+             0, (int)su, n, W2);  // A^T u_i, n x su column-major
+      launch("tucker", k_transpose_small, 1u, 256, 0, st, (const double*)Rm, b, (int)su, bc, Rt, b);
+      tall_small<double>(Vcur, n, n, bc, Rt, b, (int)su, -1.0, 1.0, W2, n, st);
       tall_tn<double>(Vacc, n, n, (int)kv, W2, n, (int)su, tpart, max_part, Cproj, st);
       tall_small<double>(Vacc, n, n, (int)std::min<int64_t>(kv, 64), Cproj, (int)kv, (int)su, -1.0,
                          1.0, W2, n, st);
@@ -553,9 +555,8 @@ static int blbp_generic(const T* A, int64_t m, int64_t n, int64_t inner, double 
   // core rows u^T a, folded into the natural layout (sketch.py:397-399)
   double* core = ar.get<double>(std::max<int64_t>(ku, 1) * n);
   TR_REQUIRE(core, "device allocation failed (out of memory?)");
-  const unsigned pg = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n * 32, 256), 16ll * num_sms()));
   for (int64_t j0 = 0; j0 < ku; j0 += 64)
-    launch("tucker", k_project_rows<T>, pg, 256, 0, st, A, m, n, (const double*)(U + m * j0),
+    launch("tucker", k_project_rows<T>, pgrid, 256, 0, st, A, m, n, (const double*)(U + m * j0),
            (int)std::min<int64_t>(ku - j0, 64), (int)j0, (int)ku, inner, core);
   *F_out = U;
   *core_out = core;

@@ -206,42 +206,6 @@ __global__ void k_gauss_block(uint64_t seed, uint64_t stream, int64_t n, int col
   }
 }
 
-// out[c * b + j] = (T) V[c + n j]: a column-major fp64 block as the row-major
-// sketch rows the panel kernels stream next to each column chunk.
-template <typename T>
-__global__ void k_rows_of(const double* __restrict__ V, int64_t n, int b, T* __restrict__ out) {
-  const int64_t total = n * b;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = e / b;
-    const int j = (int)(e % b);
-    out[e] = (T)V[c + n * j];
-  }
-}
-
-// W2[c + n j] = Wt[c * s + j] - sum_{t<bc} V[c + n t] R[j + ldr t]: the
-// bidiagonalisation's A^T u_i - v_cur r_i^T (sketch.py:334).
-template <typename T>
-__global__ void k_w2_form(const T* __restrict__ Wt, int64_t n, int s, const double* __restrict__ V,
-                          int bc, const double* __restrict__ R, int ldr, double* __restrict__ W2) {
-  __shared__ double rs[64 * 64];
-  for (int e = threadIdx.x; e < s * bc; e += blockDim.x) {
-    const int j = e % s, t = e / s;
-    rs[j + 64 * t] = R[j + (int64_t)ldr * t];
-  }
-  __syncthreads();
-  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n;
-       c += (int64_t)gridDim.x * blockDim.x) {
-    double v[64];
-    for (int t = 0; t < bc; ++t) v[t] = V[c + n * t];
-    for (int j = 0; j < s; ++j) {
-      double acc = (double)Wt[c * s + j];
-      for (int t = 0; t < bc; ++t) acc = fma(-v[t], rs[j + 64 * t], acc);
-      W2[c + n * j] = acc;
-    }
-  }
-}
-
 // Per-block sums of squares of x[0..n) (fixed order; summed by k_reduce_partials).
 template <typename T>
 __global__ void __launch_bounds__(256) k_sumsq_partial(const T* __restrict__ x, int64_t n,
@@ -317,6 +281,45 @@ __global__ void k_transpose_small(const double* __restrict__ in, int ld_in, int 
   for (int e = threadIdx.x; e < ld_out * ld_out; e += blockDim.x) {
     const int i = e % ld_out, j = e / ld_out;
     out[e] = (i < cols_in && j < rows_in) ? in[j + ld_in * i] : 0.0;
+  }
+}
+
+// partial[p][j][i] = sum_{c in split p} A[i + m c] V[c + n j] in fp64 (j < b <= B):
+// the A v pass of the bidiagonalisation with fp64 accumulation for either
+// streaming precision (its deflation test runs at 1e-10 ||A||, far below fp32
+// rounding).  One row per thread, V tiles of 32 columns in shared memory.
+template <typename T, int B>
+__global__ void __launch_bounds__(256) k_av_partial(const T* __restrict__ A, int64_t m, int64_t n,
+                                                    int b, const double* __restrict__ V,
+                                                    int64_t cols_per_split,
+                                                    double* __restrict__ partial) {
+  __shared__ double vs[32][B];
+  const int64_t row = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const int64_t cb = (int64_t)blockIdx.y * cols_per_split;
+  const int64_t ce = min(n, cb + cols_per_split);
+  double acc[B];
+#pragma unroll
+  for (int j = 0; j < B; ++j) acc[j] = 0.0;
+  for (int64_t c0 = cb; c0 < ce; c0 += 32) {
+    const int cnt = (int)(ce - c0 < 32 ? (ce - c0) : 32);
+    __syncthreads();
+    for (int e = threadIdx.x; e < 32 * B; e += 256) {
+      const int cc = e % 32, j = e / 32;
+      vs[cc][j] = (cc < cnt && j < b) ? V[c0 + cc + n * j] : 0.0;
+    }
+    __syncthreads();
+    if (row < m) {
+      const T* ap = A + row + m * c0;
+      for (int cc = 0; cc < cnt; ++cc) {
+        const double a = (double)ap[m * cc];
+#pragma unroll
+        for (int j = 0; j < B; ++j) acc[j] = fma(a, vs[cc][j], acc[j]);
+      }
+    }
+  }
+  if (row < m) {
+    double* out = partial + (int64_t)blockIdx.y * b * m;
+    for (int j = 0; j < b; ++j) out[(int64_t)j * m + row] = acc[j];
   }
 }
 

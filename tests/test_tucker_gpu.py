@@ -55,10 +55,16 @@ def test_blbp_golden_inputs_match_oracle(cuda_lib, golden, i):
         ref = lrta.gnhtsvt_randomized_blbp(a, TransformSpec("fft"), MCP, 0.3, eps, block, dtol,
                                            order, draw=lrta.PhiloxDraws(seed), canonical=True)
         assert _rel(got, ref) <= 1e-9, _rel(got, ref)
-        got32 = pk.gnhtsvt_randomized(a.astype(np.float32), pk.Transform.fft(), pk.MCP(2.5), 0.3,
-                                      sk)
+        # fp32 stream: the block Lanczos passes accumulate in fp64 (their
+        # deflation test runs at 1e-10 ||A||), so the fp32 run reproduces the
+        # oracle on the same fp32 input values
+        a32 = a.astype(np.float32)
+        got32 = pk.gnhtsvt_randomized(a32, pk.Transform.fft(), pk.MCP(2.5), 0.3, sk)
+        ref32 = lrta.gnhtsvt_randomized_blbp(a32.astype(np.float64), TransformSpec("fft"), MCP,
+                                             0.3, eps, block, dtol, order,
+                                             draw=lrta.PhiloxDraws(seed), canonical=True)
         assert got32.dtype == np.float32
-        assert _rel(got32, ref) <= 1e-4, _rel(got32, ref)
+        assert _rel(got32, ref32) <= 1e-4, _rel(got32, ref32)
 
 
 def _lowrank(dims, r, noise, seed):
