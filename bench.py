@@ -22,8 +22,10 @@ tensor is 512 MB (> 126 MB L2), so no explicit flush is needed.
 
 Multi-GPU: one process per GPU (torchrun); each rank solves its own problem
 (independent recoveries, weak scaling, no data-path collective); time = max
-over ranks.  ``--impl reference`` times the CPU oracle port of the reference
-algorithm on the host cores instead (rank 0 only).
+over ranks.  ``--impl reference`` times the reference itself (tenrec, installed
+into baseline/_ref; the oracle port when absent) on the host cores instead
+(rank 0 only): a step is one fp64 GNRHTC sweep of a 1024x1024x4 slab, and one
+sweep of the whole bench tensor is timed beside it (``full_config``).
 """
 
 from __future__ import annotations
@@ -293,8 +295,11 @@ def run_ours(args):
     # replicas: a problem per rank; sharded: the same tensor on every rank
     flat = make_workload(torch, dims, 1234 if sharded else 1234 + rank)
     cm = ColMajor(flat, dims, "torch", None)
-    sk = pk.SketchConfig(mode="fixed-rank", order=(0, 1), ranks=WORKLOAD["ranks"],
-                         blocks=WORKLOAD["blocks"], krylov=WORKLOAD["krylov"], seed=7)
+    if args.lrta == "blbp":
+        sk = pk.SketchConfig(mode="fixed-accuracy", eps=BLBP_EPS, block=BLBP_BLOCK, seed=7)
+    else:
+        sk = pk.SketchConfig(mode="fixed-rank", order=(0, 1), ranks=WORKLOAD["ranks"],
+                             blocks=WORKLOAD["blocks"], krylov=WORKLOAD["krylov"], seed=7)
     cfg = pk.SolverConfig(phi=pk.MCP(2.5), psi=pk.MCP(2.5), randomized=True, sketch=sk,
                           max_iters=max(1, args.steps))
     lam = cfg.lam_for(dims)
@@ -338,7 +343,8 @@ def run_ours(args):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     launches0 = lib.tr_launch_count()
-    lib.tr_profile_enable(1)
+    # timed region: no per-launch profiling events (they are taken afterwards,
+    # in a separate untimed pass of the same steps)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         e0.record(stream)
@@ -347,9 +353,14 @@ def run_ours(args):
         e1.record(stream)
         torch.cuda.synchronize()
     launches = lib.tr_launch_count() - launches0
+    ms = e0.elapsed_time(e1)
+    prof_steps = max(1, min(args.steps, 5))
+    lib.tr_profile_enable(1)
+    for _ in range(prof_steps):
+        step()
+    torch.cuda.synchronize()
     prof = _lib.profile_read()
     lib.tr_profile_enable(0)
-    ms = e0.elapsed_time(e1)
     if world > 1:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -425,7 +436,7 @@ def run_ours(args):
     roof = None
     if dom:
         tot_ms, n_launch = cats[dom]
-        per_step_ms = tot_ms / args.steps
+        per_step_ms = tot_ms / prof_steps
         achieved = algo[dom] / (per_step_ms / 1e3) / 1e9
         tcat, tsrc = measured_traffic()
         traffic = tcat.get(dom, {}).get("bytes_per_step")
@@ -434,9 +445,10 @@ def run_ours(args):
                 "traffic": traffic, "traffic_unit": "DRAM bytes per step (ncu, summed over launches)",
                 "traffic_source": tsrc, "share_of_step": round(per_step_ms / ms_per_step, 4),
                 "algorithmic_bytes_per_step": algo[dom],
-                "launches_per_step": n_launch / args.steps,
-                "note": "event times of the 3 concurrent mode streams overlap; uncontended "
-                        "per-kernel times are in profiles/"}
+                "launches_per_step": n_launch / prof_steps,
+                "note": "kernel time from CUDA events in a separate untimed pass of the same "
+                        "sweeps; event times of the 3 concurrent mode streams overlap; "
+                        "uncontended per-kernel times are in profiles/"}
     # The north_star's named target, the batched Krylov products, measured on
     # their own: a standalone t-SVT of the same resident tensor (one stream,
     # nothing concurrent), panel passes timed by events on their stream.
@@ -470,7 +482,12 @@ def run_ours(args):
         roof_k["how"] = ("standalone randomized t-SVT of the bench tensor (no concurrent streams); "
                          "includes the small mode-1 passes")
         del out_k
-    breakdown = {k: round(v[0] / args.steps, 4)
+    extra = {}
+    if rank == 0 and args.step == "admm" and not args.no_legs:
+        extra["fp64"] = fp64_leg(torch, pk, NativeSolver, ColMajor, lib, flat, dims, mask_dev,
+                                 min(args.steps, 10))
+        extra["blbp"] = blbp_leg(torch, pk, ColMajor, lib, cm, dims)
+    breakdown = {k: round(v[0] / prof_steps, 4)
                  for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
     if rank == 0:
         line = {
@@ -490,11 +507,78 @@ def run_ours(args):
             "roofline_krylov": roof_k,
             "kernel_ms_per_step": breakdown, "clocks": clk.summary(),
         }
+        line["config"]["lrta"] = ("block Krylov (fixed-rank BKI: ranks 25, b 7, q 3) -- BASELINE "
+                                  "configs[1] names block Lanczos bidiagonalisation; its "
+                                  "fixed-accuracy leg is the 'blbp' object" if args.lrta == "bki"
+                                  else f"block Lanczos bidiagonalisation (fixed-accuracy, "
+                                       f"eps {BLBP_EPS}, block {BLBP_BLOCK})")
+        line.update(extra)
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(args.step)
+            line["cpu_baseline"] = cpu_baseline(args.step, full=args.step == "admm")
         print(json.dumps(line), flush=True)
     if world > 1 or sharded:
         dist.destroy_process_group()
+
+
+BLBP_EPS, BLBP_BLOCK = 0.35, 8
+
+
+def fp64_leg(torch, pk, NativeSolver, ColMajor, lib, flat, dims, mask_dev, steps):
+    """The same ADMM sweep at the reference's precision (fp64 streams), timed
+    with CUDA events on the solver's stream (3 warm-up sweeps)."""
+    N = math.prod(dims)
+    cm64 = ColMajor(flat.double(), dims, "torch", None)
+    sk = pk.SketchConfig(mode="fixed-rank", order=(0, 1), ranks=WORKLOAD["ranks"],
+                         blocks=WORKLOAD["blocks"], krylov=WORKLOAD["krylov"], seed=7)
+    cfg = pk.SolverConfig(phi=pk.MCP(2.5), psi=pk.MCP(2.5), randomized=True, sketch=sk,
+                          max_iters=steps + 3)
+    run = NativeSolver("gnrhtc", cm64, None, mask_dev, cfg, WORKLOAD["modes"],
+                       cfg.lam_for(dims))
+    st = torch.cuda.ExternalStream(lib.tr_admm_stream(run.handle))
+    for _ in range(3):
+        run.step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        run.step()
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    run.close()
+    del cm64
+    torch.cuda.empty_cache()
+    return {"dtype": "f64", "value": len(WORKLOAD["modes"]) * N / (ms / 1e3), "unit": UNIT,
+            "ms_per_step": ms, "steps": steps, "warmup": 3,
+            "how": "same workload and sweep, fp64 tensors (the reference's precision), CUDA "
+                   "events on the solver stream"}
+
+
+def blbp_leg(torch, pk, ColMajor, lib, cm, dims, reps=3):
+    """One fixed-accuracy (block Lanczos, sketch.py:287-403) randomized t-SVT of
+    the bench tensor through the public API, device-resident input."""
+    N = math.prod(dims)
+    sk = pk.SketchConfig(mode="fixed-accuracy", eps=BLBP_EPS, block=BLBP_BLOCK, seed=7)
+    tau = 0.05 * float(cm.flat.norm()) / math.sqrt(N)
+    pk.gnhtsvt_randomized(cm, pk.Transform.fft(), pk.MCP(2.5), tau, sk)
+    torch.cuda.synchronize()
+    launches0 = lib.tr_launch_count()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        out = pk.gnhtsvt_randomized(cm, pk.Transform.fft(), pk.MCP(2.5), tau, sk)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / reps
+    launches = (lib.tr_launch_count() - launches0) / reps
+    del out
+    _, diag = pk.ad_rsthosvd_blbp(cm, BLBP_EPS, block=BLBP_BLOCK, order=(0, 1), seed=7)
+    torch.cuda.empty_cache()
+    return {"value": N / dt, "unit": UNIT, "ms_per_tsvt": dt * 1e3, "eps": BLBP_EPS,
+            "block": BLBP_BLOCK, "ranks": [diag.ranks[0], diag.ranks[1]],
+            "iterations": [diag.iterations[0], diag.iterations[1]],
+            "deflations": [diag.deflations[0], diag.deflations[1]],
+            "launches_per_tsvt": launches,
+            "how": "wall clock of the host-driven call (two small D2H per bidiagonalisation "
+                   "step), device-resident input"}
 
 
 def _threads():
@@ -522,14 +606,98 @@ def _slab(nf, seed):
     return flat.reshape(x.shape)
 
 
-def cpu_baseline(step="admm", nf=8, seed=0, iters=1):
-    """The oracle port (numpy restatement of tenrec) timed on the host cores on a
-    bounded sample: ``iters`` ADMM sweeps (or one t-SVT) of a 1024x1024x``nf`` slab."""
+def _tenrec():
+    """The unmodified reference package, installed once into baseline/_ref
+    ("Reference arm"); None when it is absent."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "tenrec")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import tenrec
+        return tenrec
+    except Exception:
+        return None
+
+
+def tenrec_sweeps(tenrec, x, iters=1):
+    """Seconds of ``iters`` GNRHTC sweeps of the reference itself: the loop body
+    of tenrec/solvers.py:226-268 composed from tenrec's public functions
+    (solve_grad_system, grad, gnhtsvt_randomized with the bench sketch, gnhtt,
+    kkt_diagnostics) in the reference's order.  The end-of-solve objective
+    (full face SVDs, solvers.py:274-282) is per solve, not per sweep, and is
+    not timed."""
+    import numpy as np
+
+    dims = x.shape
+    modes = WORKLOAD["modes"]
+    sk = tenrec.SketchConfig(mode="fixed-rank", order=(0, 1), ranks=WORKLOAD["ranks"],
+                             blocks=WORKLOAD["blocks"], krylov=WORKLOAD["krylov"], seed=7)
+    cfg = tenrec.SolverConfig(phi=tenrec.MCP(2.5), psi=tenrec.MCP(2.5), randomized=True,
+                              sketch=sk, tol=1e-30, max_iters=iters)
+    gset = tenrec.GradientSet(dims, modes)
+    lam = cfg.lam_for(dims)
+    gamma = len(modes)
+    maskf = np.ones(dims)
+    zeros = lambda: np.zeros(dims)  # noqa: E731
+    l, e, y = zeros(), zeros(), zeros()
+    g = {k: zeros() for k in modes}
+    lag = {k: zeros() for k in modes}
+    mu = cfg.mu0
+    t0 = time.perf_counter()
+    for _ in range(iters):
+        b = x - e + y / mu
+        l_new = tenrec.solve_grad_system(b, {k: g[k] - lag[k] / mu for k in modes}, gset)
+        tau = 1.0 / (gamma * mu)
+        grad_l = {k: tenrec.grad(l_new, k) for k in modes}
+        g_new = {k: tenrec.gnhtsvt_randomized(grad_l[k] + lag[k] / mu, cfg.transform, cfg.phi,
+                                              tau, cfg.sketch) for k in modes}
+        h = x - l_new + y / mu
+        e_new = maskf * tenrec.gnhtt(maskf * h, cfg.psi, lam / mu, cfg.structure) \
+            + (1.0 - maskf) * h
+        y = y + mu * (x - l_new - e_new)
+        for k in modes:
+            lag[k] = lag[k] + mu * (grad_l[k] - g_new[k])
+        tenrec.kkt_diagnostics(tenrec.SolverState(m=x, l=l_new, e=e_new, g=g_new, grad_l=grad_l,
+                                                  l_prev=l, e_prev=e, g_prev=g))
+        l, e, g = l_new, e_new, g_new
+        mu = min(cfg.mu_max, cfg.growth * mu)
+    return time.perf_counter() - t0
+
+
+def _full_config_x():
+    """The bench tensor itself (bench.make_workload, seed 1234) as fp64 numpy,
+    generated on the GPU when one is visible, else the slab generator."""
+    import numpy as np
+
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            dims = WORKLOAD["dims"]
+            flat = make_workload(torch, dims, 1234)
+            x = flat.reshape(tuple(reversed(dims))).permute(2, 1, 0).cpu().numpy()
+            del flat
+            torch.cuda.empty_cache()
+            return np.asfortranarray(x, dtype=np.float64)
+    except Exception:
+        pass
+    return _slab(WORKLOAD["dims"][2], 1234)
+
+
+def cpu_baseline(step="admm", nf=8, seed=0, iters=1, full=False):
+    """The reference timed on the host cores on a bounded sample: ``iters``
+    GNRHTC sweeps (or one t-SVT) of a 1024x1024x``nf`` slab.  tenrec itself
+    (baseline/_ref, kind "reference") when installed, else the oracle port.
+    ``full``: one sweep of the whole 1024x1024x128 bench tensor beside it, which
+    checks the per-voxel extrapolation from the slab."""
     import numpy as np
 
     from oracle import admm, lrta, philox
     from oracle.tensor_ops import TransformSpec
 
+    tenrec = _tenrec()
     x = _slab(nf, seed)
     spec = TransformSpec("fft")
     mcp = (2, 2.5, 0.0)
@@ -538,20 +706,41 @@ def cpu_baseline(step="admm", nf=8, seed=0, iters=1):
         return lrta.gnhtsvt_randomized(a, spec, mcp, tau, WORKLOAD["ranks"], WORKLOAD["blocks"],
                                        WORKLOAD["krylov"], (0, 1), philox.PhiloxSketchSource(7))
 
-    t0 = time.perf_counter()
+    kind = "reference" if tenrec is not None else "port"
+    who = "tenrec 0.1.0 (baseline/_ref)" if tenrec is not None else "fp64 numpy oracle port"
     if step == "admm":
-        mask = np.ones(x.shape, dtype=bool)
-        admm.admm_complete(x, mask, thr, mcp, admm.default_lambda(x.shape), WORKLOAD["modes"],
-                           max_iters=iters, tol=1e-30)
-        vox = 3 * x.size * iters
-        sample = f"{iters} GNRHTC sweep(s) of a 1024x1024x{nf} slab (fp64 numpy oracle)"
+        if tenrec is not None:
+            dt = tenrec_sweeps(tenrec, x, iters)
+        else:
+            t0 = time.perf_counter()
+            admm.admm_complete(x, np.ones(x.shape, dtype=bool), thr, mcp,
+                               admm.default_lambda(x.shape), WORKLOAD["modes"], max_iters=iters,
+                               tol=1e-30)
+            dt = time.perf_counter() - t0
+        vox = len(WORKLOAD["modes"]) * x.size * iters
+        sample = f"{iters} GNRHTC sweep(s) of a 1024x1024x{nf} slab ({who}, fp64)"
     else:
-        thr(x, 0.05)
+        t0 = time.perf_counter()
+        if tenrec is not None:
+            sk = tenrec.SketchConfig(mode="fixed-rank", order=(0, 1), ranks=WORKLOAD["ranks"],
+                                     blocks=WORKLOAD["blocks"], krylov=WORKLOAD["krylov"], seed=7)
+            tenrec.gnhtsvt_randomized(x, tenrec.Transform.fft(), tenrec.MCP(2.5), 0.05, sk)
+        else:
+            thr(x, 0.05)
+        dt = time.perf_counter() - t0
         vox = x.size
-        sample = f"one randomized t-SVT of a 1024x1024x{nf} slab (fp64 numpy oracle)"
-    dt = time.perf_counter() - t0
-    return {"value": vox / dt, "unit": UNIT, "cores": _threads(), "kind": "port",
-            "sample": sample, "seconds": dt}
+        sample = f"one randomized t-SVT of a 1024x1024x{nf} slab ({who}, fp64)"
+    out = {"value": vox / dt, "unit": UNIT, "cores": _threads(), "kind": kind,
+           "sample": sample, "seconds": dt}
+    if full and step == "admm" and tenrec is not None:
+        xf = _full_config_x()
+        dtf = tenrec_sweeps(tenrec, xf, 1)
+        out["full_config"] = {
+            "value": len(WORKLOAD["modes"]) * xf.size / dtf, "unit": UNIT, "seconds": dtf,
+            "sample": "1 GNRHTC sweep of the whole 1024x1024x128 bench tensor (tenrec, fp64)",
+            "slab_extrapolation_ratio": (vox / dt) / (len(WORKLOAD["modes"]) * xf.size / dtf)}
+        del xf
+    return out
 
 
 def run_reference(args):
@@ -559,15 +748,18 @@ def run_reference(args):
     rank = _env_int("RANK", 0)
     if rank != 0:
         return
+    nf = 4
     for w in range(args.warmup):
-        cpu_baseline(args.step, nf=4, seed=100 + w)
+        cpu_baseline(args.step, nf=nf, seed=100 + w)
     vals, secs = [], 0.0
     for s in range(args.steps):
-        r = cpu_baseline(args.step, nf=4, seed=s)
+        r = cpu_baseline(args.step, nf=nf, seed=s)
         vals.append(r["value"])
         secs += r["seconds"]
     value = statistics.mean(vals)
     sample = r["sample"]
+    full = cpu_baseline(args.step, nf=nf, seed=0, full=True).get("full_config") \
+        if not args.no_cpu_baseline else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * secs / max(args.steps, 1),
@@ -576,10 +768,12 @@ def run_reference(args):
         "impl": "reference",
         "config": {"workload": WORKLOAD["workload"], "step": args.step,
                    "sample": "per step: " + sample},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": _threads(), "kind": "port",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": _threads(), "kind": r["kind"],
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if full:
+        line["full_config"] = full
     print(json.dumps(line), flush=True)
 
 
@@ -591,6 +785,10 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--step", choices=("admm", "lrta", "tsvt-sharded"), default="admm")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-legs", action="store_true", help="skip the fp64 and BLBP legs")
+    ap.add_argument("--lrta", choices=("bki", "blbp"), default="bki",
+                    help="sketch of the ADMM step's t-SVTs: fixed-rank block Krylov (default) "
+                         "or fixed-accuracy block Lanczos")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
