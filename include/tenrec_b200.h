@@ -192,6 +192,46 @@ int tr_admm_create(int dtype, int order, const int64_t* dims, int kind, const vo
 int tr_admm_step(void* handle, double* out);
 int tr_admm_read(void* handle, int which, void* dst, void* stream);
 int tr_admm_destroy(void* handle);
+/*
+ * Multi-GPU ADMM (BASELINE configs[4]; north_star's sharded solve): rank `rank`
+ * of `world` holds faces [last_off, last_off + dims[order-1]) of the LAST mode
+ * (length last_all = world * dims[order-1]); `dims` are the local dims and
+ * obs_a / mask the local slabs.  Per sweep: the FFT-diagonal L-solve runs the
+ * local axes in place and the last axis after an all-to-all transpose (each
+ * rank then owns whole last-axis lines of 1/world of the spectrum) and back;
+ * the circular stencils along the last axis read one ghost face per
+ * neighbour (halo exchange of L, the last mode's G and multiplier); every
+ * t-SVT is the last-mode-sharded one of tr_gnhtsvt_randomized_sharded (fp64
+ * all-reduces of the Krylov blocks, Ritz Gram and core); the Eq. (24)
+ * residuals are all-reduced (sum / max) so tr_admm_step returns the global
+ * values on every rank.  GNRHTC / GNHTC, entry-wise noise, randomized
+ * fixed-rank sketch of modes (0, 1), FFT transform.  The collectives are the
+ * caller's, ordered on `stream` (e.g. NCCL through torch.distributed):
+ *   allreduce  in-place fp64 over `count` values, op 0 sum / 1 max
+ *   alltoall   `bytes` from send + q*bytes go to rank q, recv + q*bytes
+ *              come from rank q
+ *   halo       send first_face to rank-1 and last_face to rank+1 (ring);
+ *              receive rank-1's last face into ghost_prev and rank+1's first
+ *              face into ghost_next (`bytes` each)
+ * world == 1 needs no callbacks (the exchanges are local copies).
+ */
+typedef struct tr_comm {
+  int world, rank;
+  int (*allreduce)(double* buf, int64_t count, int op, void* stream, void* user);
+  int (*alltoall)(const void* send, void* recv, int64_t bytes, void* stream, void* user);
+  int (*halo)(const void* first_face, const void* last_face, void* ghost_prev, void* ghost_next,
+              int64_t bytes, void* stream, void* user);
+  void* user;
+} tr_comm;
+int tr_admm_create_sharded(int dtype, int order, const int64_t* dims, int kind,
+                           const void* obs_a, const uint8_t* mask, int nmodes,
+                           const int64_t* modes, int phi_kind, double phi_p0, double phi_p1,
+                           int psi_kind, double psi_p0, double psi_p1, double lam, double mu0,
+                           double mu_max, double growth, const int64_t* ranks,
+                           const int64_t* blocks, const int64_t* krylov, uint64_t seed,
+                           int64_t last_all, int64_t last_off, const tr_comm* comm,
+                           void** handle);
+
 /* Route the solver's t-SVTs through the generic Tucker engine (tr_tucker_*)
  * with this sketch: any processing order, fixed-rank (sketch_mode 0) or
  * fixed-accuracy block Lanczos (sketch_mode 1); arguments as tr_tucker_create.

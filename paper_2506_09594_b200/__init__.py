@@ -12,7 +12,8 @@ from .penalties import (PENALTY_NAMES, L1, MCP, SCAD, CappedLq, Firm, LogPenalty
 from .gradient import GradientSet, solve_grad_system
 from .onebit import (ObservationSet, data_fit_update, gnobhtc, gnobrhtc, naive_estimate,
                      onebit_observe)
-from .shard import DeviceAllreduce, gnhtsvt_randomized_sharded, shard_range
+from .shard import (DeviceAllreduce, DeviceComm, gnhtc_sharded, gnhtsvt_randomized_sharded,
+                    gnrhtc_sharded, shard_range)
 from .sketch import (BLBPDiagnostics, SketchConfig, TuckerFactors, ad_rsthosvd_blbp,
                      gnhtsvt_randomized, rsthosvd_bki)
 from .solvers import SolveReport, SolverConfig, default_lambda, gnhtc, gnrhtc
@@ -27,4 +28,5 @@ __all__ = [
     "DEFAULT_TRANSFORM", "Transform", "TransformError", "SolveReport", "SolverConfig",
     "default_lambda", "gnhtc", "gnrhtc", "ObservationSet", "data_fit_update", "gnobhtc",
     "gnobrhtc", "naive_estimate", "onebit_observe", "GradientSet", "solve_grad_system", "DeviceAllreduce", "gnhtsvt_randomized_sharded", "shard_range",
+    "DeviceComm", "gnrhtc_sharded", "gnhtc_sharded",
 ]

@@ -24,6 +24,23 @@ _vp = ctypes.c_void_p
 ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_int64,
                                 ctypes.c_void_p, ctypes.c_void_p)
 
+# the tr_comm collectives of the sharded ADMM
+COMM_ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_int64,
+                                     ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p)
+COMM_ALLTOALL_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                    ctypes.c_void_p, ctypes.c_void_p)
+COMM_HALO_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p)
+
+
+class TrComm(ctypes.Structure):
+    """struct tr_comm (include/tenrec_b200.h)."""
+
+    _fields_ = [("world", ctypes.c_int), ("rank", ctypes.c_int),
+                ("allreduce", COMM_ALLREDUCE_FN), ("alltoall", COMM_ALLTOALL_FN),
+                ("halo", COMM_HALO_FN), ("user", ctypes.c_void_p)]
+
+
 # name -> (restype, argtypes); the list is the contract tests check against the header
 SIGNATURES = {
     "tr_version": (ctypes.c_int, []),
@@ -49,6 +66,12 @@ SIGNATURES = {
         ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
         _c_i64p, _c_i64p, _c_i64p, ctypes.c_uint64, ctypes.c_int, _vp, _c_dp,
         ctypes.POINTER(ctypes.c_void_p)]),
+    "tr_admm_create_sharded": (ctypes.c_int, [
+        ctypes.c_int, ctypes.c_int, _c_i64p, ctypes.c_int, _vp, _vp, ctypes.c_int, _c_i64p,
+        ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_double,
+        ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+        _c_i64p, _c_i64p, _c_i64p, ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64,
+        ctypes.POINTER(TrComm), ctypes.POINTER(ctypes.c_void_p)]),
     "tr_admm_step": (ctypes.c_int, [_vp, _c_dp]),
     "tr_admm_read": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp]),
     "tr_admm_destroy": (ctypes.c_int, [_vp]),

@@ -85,6 +85,18 @@ struct Solver {
   double mu;
   int64_t red_blocks;
   std::vector<void*> allocs;
+  // multi-GPU: this rank holds faces [last_off, last_off + nl) of the last axis
+  // (length last_all); stencils along it read ghost faces (Geom::halo), the FFT
+  // solve transposes the last axis in with an all-to-all (fft_solve_dist), the
+  // t-SVTs all-reduce their Krylov blocks / Gram / core (lrta.cu), and the
+  // Eq. (24) residuals are all-reduced before they reach the host.
+  bool sharded = false;
+  tr_comm comm{};
+  int64_t last_all = 0, last_off = 0, nl = 0, face = 0;
+  cpx<T>* spec_pack = nullptr;
+  cpx<T>* spec_recv = nullptr;
+  double* res_max = nullptr;
+  double* hres_max = nullptr;
 
   template <typename X_>
   X_* alloc(int64_t n) {
@@ -93,9 +105,17 @@ struct Solver {
     allocs.push_back(p);
     return (X_*)p;
   }
+  // N own elements plus a ghost face on each side when sharded (pointer to own
+  // element 0)
+  T* alloc_ghosted(int64_t n) {
+    if (!sharded) return alloc<T>(n);
+    T* p = alloc<T>(n + 2 * face);
+    return p ? p + face : nullptr;
+  }
   ~Solver() {
     for (void* p : allocs) cudaFreeAsync(p, 0);
     if (hres) cudaFreeHost(hres);
+    if (hres_max) cudaFreeHost(hres_max);
     for (auto s : streams) cudaStreamDestroy(s);
     for (auto e : evs) cudaEventDestroy(e);
     if (ev_main) cudaEventDestroy(ev_main);
@@ -350,6 +370,119 @@ static int fft_solve2(Solver<T>& s, const T* rhs, T* out, cudaStream_t st) {
   return 0;
 }
 
+// Multi-GPU FFT solve: the local axes as in fft_solve2, the sharded last axis
+// through an all-to-all transpose.  The local half spectrum is lo (M, every
+// axis before the last) x nl faces; rank q receives lo chunk q (M / W
+// elements) of every rank's faces, i.e. whole last-axis lines, solves them,
+// and the inverse all-to-all restores the slab layout.
+template <typename T>
+static int fft_solve_dist(Solver<T>& s, const T* rhs, T* out, cudaStream_t st) {
+  const Geom& g = s.g;
+  const int d = g.d;
+  const int64_t n0 = g.dims[0], n1 = g.dims[1];
+  const int hn = (int)(n0 / 2);
+  TR_REQUIRE(n0 % 2 == 0 && (hn & (hn - 1)) == 0 && hn >= 8 && hn <= 2048 &&
+                 (n0 * (int64_t)sizeof(T)) % 16 == 0,
+             "sharded FFT solve needs an even power-of-two first mode in [16, 4096]");
+  const int W = s.comm.world;
+  int64_t sd[kMaxOrder], sst[kMaxOrder];
+  int orig[kMaxOrder];
+  sd[0] = n1;
+  orig[0] = 1;
+  sd[1] = hn + 1;
+  orig[1] = 0;
+  for (int a = 2; a < d; ++a) {
+    sd[a] = g.dims[a];
+    orig[a] = a;
+  }
+  int64_t SN = 1;
+  for (int a = 0; a < d; ++a) {
+    sst[a] = SN;
+    SN *= sd[a];
+  }
+  const int64_t M = sst[d - 1];
+  TR_REQUIRE(M % W == 0, "sharded FFT solve: %lld spectrum lines do not split over %d ranks",
+             (long long)M, W);
+  const int64_t mw = M / W, nl = s.nl;
+  SolveSpec off = s.ss, on = s.ss;
+  off.active = 0;
+  on.active = 1;
+  for (int p = 0; p < d; ++p) {
+    off.dims[p] = on.dims[p] = sd[p];
+    off.lam_off[p] = on.lam_off[p] = s.ss.lam_off[orig[p]];
+  }
+  on.dims[d - 1] = s.last_all;
+  on.lo_base = (int64_t)s.comm.rank * mw;
+  const cpx<T>* const* tw = (const cpx<T>* const*)s.tw.data();
+  const int64_t lines = g.N / n0;
+  fft_pass_p2<T>(FFT_R2C, rhs, s.spec, 1.0, 1, (int)n0, lines, tw[0], 0, off, (const double*)s.lam,
+                 n1, st);
+  for (int p = 0; p < d - 1; ++p) {
+    if (p == 1) continue;
+    if (fft_c2c<T>(tw[orig[p]], s.lam, s.spec, (int)sd[p], sst[p], SN / (sst[p] * sd[p]), 0, off, st))
+      return 1;
+  }
+  const size_t es = sizeof(cpx<T>);
+  for (int q = 0; q < W; ++q)  // pack: lo chunk q of every own face, contiguous per rank
+    TR_CUDA(cudaMemcpy2DAsync(s.spec_pack + q * mw * nl, mw * es, s.spec + q * mw, M * es, mw * es,
+                              nl, cudaMemcpyDeviceToDevice, st));
+  TR_LAUNCH_CHECK();
+  if (W == 1) {
+    TR_CUDA(cudaMemcpyAsync(s.spec_recv, s.spec_pack, es * M * nl, cudaMemcpyDeviceToDevice, st));
+  } else {
+    TR_REQUIRE(s.comm.alltoall(s.spec_pack, s.spec_recv, (int64_t)(es * mw * nl), (void*)st,
+                               s.comm.user) == 0, "all-to-all callback failed");
+  }
+  // whole last-axis lines: forward, solve, inverse (stride mw, one line group)
+  if (fft_c2c<T>(tw[d - 1], s.lam, s.spec_recv, (int)s.last_all, mw, 1, 0, on, st)) return 1;
+  if (W == 1) {
+    TR_CUDA(cudaMemcpyAsync(s.spec_pack, s.spec_recv, es * M * nl, cudaMemcpyDeviceToDevice, st));
+  } else {
+    TR_REQUIRE(s.comm.alltoall(s.spec_recv, s.spec_pack, (int64_t)(es * mw * nl), (void*)st,
+                               s.comm.user) == 0, "all-to-all callback failed");
+  }
+  for (int q = 0; q < W; ++q)  // unpack lo chunk q
+    TR_CUDA(cudaMemcpy2DAsync(s.spec + q * mw, M * es, s.spec_pack + q * mw * nl, mw * es, mw * es,
+                              nl, cudaMemcpyDeviceToDevice, st));
+  for (int p = d - 2; p >= 0; --p) {
+    if (p == 1) continue;
+    if (fft_c2c<T>(tw[orig[p]], s.lam, s.spec, (int)sd[p], sst[p], SN / (sst[p] * sd[p]), 1, off, st))
+      return 1;
+  }
+  fft_pass_p2<T>(FFT_C2R, s.spec, out, 2.0 / (double)(g.N / nl * s.last_all), 1, (int)n0, lines,
+                 tw[0], 0, off, (const double*)s.lam, n1, st);
+  TR_LAUNCH_CHECK();
+  return 0;
+}
+
+// Ghost faces of a sharded array along the last axis: the previous rank's last
+// own face -> ghost_prev, the next rank's first own face -> ghost_next (ring,
+// the gradients are circular).  `both` = false fills ghost_prev only.
+template <typename T>
+static int halo_exchange(Solver<T>& s, T* x, cudaStream_t st) {
+  const int64_t f = s.face;
+  T* first = x;
+  T* last = x + (s.nl - 1) * f;
+  T* gprev = x - f;
+  T* gnext = x + s.nl * f;
+  if (s.comm.world == 1) {
+    TR_CUDA(cudaMemcpyAsync(gprev, last, sizeof(T) * f, cudaMemcpyDeviceToDevice, st));
+    TR_CUDA(cudaMemcpyAsync(gnext, first, sizeof(T) * f, cudaMemcpyDeviceToDevice, st));
+    return 0;
+  }
+  TR_REQUIRE(s.comm.halo(first, last, gprev, gnext, (int64_t)(sizeof(T) * f), (void*)st,
+                         s.comm.user) == 0,
+             "halo exchange callback failed");
+  return 0;
+}
+
+// the t-SVT's in-place fp64 sum (tr_allreduce_fn) over the solver's comm
+static int comm_allreduce_sum(double* buf, int64_t count, void* stream, void* user) {
+  const tr_comm* c = (const tr_comm*)user;
+  if (c->world == 1) return 0;
+  return c->allreduce(buf, count, 0, stream, c->user);
+}
+
 // deterministic t-SVT of a whole tensor with small faces (n1, n2 <= 64)
 template <typename T>
 static int full_svt(Solver<T>& s, const T* X, T* out, double tau, void* ws, cudaStream_t st) {
@@ -503,6 +636,7 @@ static int admm_step(Solver<T>& s, double* hout) {
   // fused sweep tail (lag + noise/dual + next rhs in one pass): gradient chain,
   // <= 4 modes, vector path
   const bool fuse = !s.onebit() && !pure && nm <= 4 && v4 && !s.lag2.empty();
+  TR_REQUIRE(!s.sharded || fuse, "the sharded solver needs the fused sweep tail (aligned buffers)");
   if (!fuse) s.rhs_ready = false;
   const auto rhs_k = v4 ? k_admm_rhs<T, 4> : k_admm_rhs<T, 1>;
   double* part = s.part;
@@ -518,7 +652,12 @@ static int admm_step(Solver<T>& s, double* hout) {
     } else {
       if (!s.rhs_ready)
         launch("admm_rhs", rhs_k, grid, kRedThreads, 0, st, g, s.A, s.e, s.y, mu, gp, lp, s.rhs);
-      if (fft_solve2<T>(s, s.rhs, s.l, st)) return 1;
+      if (s.sharded) {
+        if (fft_solve_dist<T>(s, s.rhs, s.l, st)) return 1;
+        if (halo_exchange<T>(s, s.l, st)) return 1;  // grad along the last axis
+      } else if (fft_solve2<T>(s, s.rhs, s.l, st)) {
+        return 1;
+      }
     }
     tau = 1.0 / (gamma * mu);
     lrta_inputs<T>(s, s.l, mu, v4, grid, st);
@@ -567,6 +706,9 @@ static int admm_step(Solver<T>& s, double* hout) {
           if (overlap) noise_dual();
         }))
       return 2;
+    if (s.sharded)  // D_last^T G_new in the next right-hand side
+      for (int k = 0; k < nm; ++k)
+        if (s.cfg.modes[k] == g.d - 1 && halo_exchange<T>(s, s.gnew[k], st)) return 1;
     if (!fuse) lag_updates<T>(s, s.l, mu, v4, grid, st);
     if (!overlap && fuse) group_scale();
     if (fuse) {
@@ -608,6 +750,9 @@ static int admm_step(Solver<T>& s, double* hout) {
              res + 96);
       for (int k = 0; k < nm; ++k) std::swap(s.lag[k], s.lag2[k]);
       s.rhs_ready = true;
+      if (s.sharded)  // the next tail recomputes the previous face's multiplier
+        for (int k = 0; k < nm; ++k)
+          if (s.cfg.modes[k] == g.d - 1 && halo_exchange<T>(s, s.lag[k], st)) return 1;
     } else {
       noise_dual();
     }
@@ -644,8 +789,26 @@ static int admm_step(Solver<T>& s, double* hout) {
     lag_updates<T>(s, s.z, mu, v4, grid, st);
   }
   TR_LAUNCH_CHECK();
+  if (s.sharded && s.comm.world > 1) {
+    // residual slots are sums (squares) or maxima (inf-norms): reduce both ways
+    TR_CUDA(cudaMemcpyAsync(s.res_max, res, 128 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    TR_REQUIRE(s.comm.allreduce(res, 128, 0, (void*)st, s.comm.user) == 0 &&
+                   s.comm.allreduce(s.res_max, 128, 1, (void*)st, s.comm.user) == 0,
+               "residual all-reduce callback failed");
+    TR_CUDA(cudaMemcpyAsync(s.hres_max, s.res_max, 128 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  }
   TR_CUDA(cudaMemcpyAsync(s.hres, res, 128 * sizeof(double), cudaMemcpyDeviceToHost, st));
   TR_CUDA(cudaStreamSynchronize(st));
+  if (s.sharded && s.comm.world > 1) {
+    // fused layout (the only sharded one): per mode [grad max, grad^2, dG max,
+    // dG^2, lag^2] at 96 + 5k, noise [dL max, dL^2, dE max, dE^2, fit max,
+    // fit^2, Y^2] at 116
+    for (int k = 0; k < nm; ++k) {
+      s.hres[96 + 5 * k + 0] = s.hres_max[96 + 5 * k + 0];
+      s.hres[96 + 5 * k + 2] = s.hres_max[96 + 5 * k + 2];
+    }
+    for (int i : {0, 2, 4}) s.hres[116 + i] = s.hres_max[116 + i];
+  }
   const double* h = s.hres;
   const double* hl = fuse ? h + 96 : h;          // per-mode multiplier residuals
   const double* hn = (fuse && !overlap_noise) ? h + 96 + 20 : h + 64;  // noise / dual residuals
@@ -688,13 +851,38 @@ static int admm_step(Solver<T>& s, double* hout) {
 
 template <typename T>
 static int admm_create(const AdmmConfig& cfg, int order, const int64_t* dims, const void* a,
-                       const void* b, const uint8_t* mask, Solver<T>** out) {
+                       const void* b, const uint8_t* mask, Solver<T>** out,
+                       const tr_comm* comm = nullptr, int64_t last_all = 0,
+                       int64_t last_off = 0) {
   TR_REQUIRE(order >= 3 && order <= kMaxOrder, "order must be in [3, %d]", kMaxOrder);
   TR_REQUIRE(cfg.nmodes >= 1 && cfg.nmodes <= kMaxOrder, "need 1..%d gradient modes", kMaxOrder);
+  if (comm) {
+    TR_REQUIRE(comm->world >= 1 && comm->rank >= 0 && comm->rank < comm->world,
+               "bad communicator (rank %d of %d)", comm->rank, comm->world);
+    TR_REQUIRE(comm->world == 1 || (comm->allreduce && comm->alltoall && comm->halo),
+               "a multi-rank solver needs allreduce, alltoall and halo callbacks");
+    TR_REQUIRE(cfg.kind <= 1 && cfg.randomized, "the sharded solver runs GNRHTC / GNHTC with a "
+               "randomized sketch");
+    TR_REQUIRE(cfg.structure == 0, "the sharded solver supports entry-wise noise shrinkage");
+    TR_REQUIRE(cfg.nmodes <= 4 && cfg.modes[0] >= 0 && dims[0] % 4 == 0,
+               "the sharded solver needs <= 4 gradient modes and a first mode divisible by 4");
+    TR_REQUIRE(last_all == dims[order - 1] * comm->world &&
+                   last_off == dims[order - 1] * comm->rank,
+               "the last mode must split evenly: rank %d of %d owns [%lld, %lld) of %lld", comm->rank,
+               comm->world, (long long)last_off, (long long)(last_off + dims[order - 1]),
+               (long long)last_all);
+  }
   TR_CUDA(cudaDeviceSynchronize());  // inputs written on the caller's streams
   auto* s = new Solver<T>();
   s->cfg = cfg;
   s->order = order;
+  if (comm) {
+    s->sharded = true;
+    s->comm = *comm;
+    s->last_all = last_all;
+    s->last_off = last_off;
+    s->nl = dims[order - 1];
+  }
   Geom& g = s->g;
   g.d = order;
   g.N = 1;
@@ -706,10 +894,23 @@ static int admm_create(const AdmmConfig& cfg, int order, const int64_t* dims, co
   }
   const int64_t N = g.N;
   const int nm = cfg.nmodes;
+  if (s->sharded) {
+    g.halo = order - 1;
+    s->face = N / s->nl;
+  }
   if (cfg.randomized) {
     if (make_shape(order, dims, cfg.ranks, cfg.blocks, cfg.krylov, s->sh)) {
       delete s;
       return 1;
+    }
+    if (s->sharded) {  // the t-SVT of a last-mode shard (lrta.cu, tr_gnhtsvt_randomized_sharded)
+      Shape& sh = s->sh;
+      const int64_t inner = sh.nf / s->nl;
+      sh.tr.d[order - 3] = last_all;
+      sh.nf_all = inner * last_all;
+      sh.f0 = inner * last_off;
+      sh.coll = s->comm.world > 1 ? comm_allreduce_sum : nullptr;
+      sh.coll_user = &s->comm;
     }
   } else {
     if (!(dims[0] <= 4096 && dims[1] <= 4096)) {
@@ -735,26 +936,39 @@ static int admm_create(const AdmmConfig& cfg, int order, const int64_t* dims, co
   s->B = (const T*)b;
   s->mask = mask;
   s->mu = cfg.mu0;
-  s->l = s->template alloc<T>(N);
-  s->lold = s->template alloc<T>(N);
+  // arrays a stencil reads along the sharded last axis carry ghost faces
+  auto on_last = [&](int k) { return s->sharded && cfg.modes[k] == order - 1; };
+  auto big = [&](bool ghost) { return ghost ? s->alloc_ghosted(N) : s->template alloc<T>(N); };
+  s->l = big(s->sharded);
+  s->lold = big(s->sharded);
   s->e = s->template alloc<T>(N);
   s->y = s->template alloc<T>(N);
   s->z = s->template alloc<T>(N);
   s->rhs = s->template alloc<T>(N);
   for (int k = 0; k < nm; ++k) {
-    s->gcur.push_back(s->template alloc<T>(N));
-    s->gnew.push_back(s->template alloc<T>(N));
-    s->lag.push_back(s->template alloc<T>(N));
+    s->gcur.push_back(big(on_last(k)));
+    s->gnew.push_back(big(on_last(k)));
+    s->lag.push_back(big(on_last(k)));
     s->X.push_back(s->template alloc<T>(N));
   }
   // second multiplier buffers for the fused sweep tail (gradient chain, <= 4 modes)
-  if (cfg.kind < 2 && nm <= 4 && cfg.modes[0] >= 0 && getenv("TR_NO_FUSE") == nullptr)
-    for (int k = 0; k < nm; ++k) s->lag2.push_back(s->template alloc<T>(N));
+  if (cfg.kind < 2 && nm <= 4 && cfg.modes[0] >= 0 &&
+      (s->sharded || getenv("TR_NO_FUSE") == nullptr))
+    for (int k = 0; k < nm; ++k) s->lag2.push_back(big(on_last(k)));
   s->spec = s->template alloc<cpx<T>>(N);
+  if (s->sharded) {
+    s->spec_pack = s->template alloc<cpx<T>>(N);
+    s->spec_recv = s->template alloc<cpx<T>>(N);
+    s->res_max = s->template alloc<double>(128);
+  }
+  // global axis lengths (the FFT twiddles and Laplacian tables of the last
+  // axis span every rank's faces)
+  int64_t gd[kMaxOrder];
+  for (int i = 0; i < order; ++i) gd[i] = (s->sharded && i == order - 1) ? last_all : dims[i];
   int64_t lam_total = 0;
   for (int i = 0; i < order; ++i) {
-    s->tw.push_back(s->template alloc<cpx<T>>(dims[i]));
-    lam_total += dims[i];
+    s->tw.push_back(s->template alloc<cpx<T>>(gd[i]));
+    lam_total += gd[i];
   }
   s->lam = s->template alloc<double>(lam_total);
   s->scale = s->template alloc<double>(std::max<int64_t>(dims[0] * dims[1], N / (dims[0] * dims[1])));
@@ -768,6 +982,7 @@ static int admm_create(const AdmmConfig& cfg, int order, const int64_t* dims, co
     }
   TR_CUDA(cudaStreamSynchronize(0));  // pool allocations are ordered on the legacy stream
   TR_CUDA(cudaMallocHost(&s->hres, 128 * sizeof(double)));
+  if (s->sharded) TR_CUDA(cudaMallocHost(&s->hres_max, 128 * sizeof(double)));
   // LRTA workspaces, one per mode stream
   {
     Carve cv(nullptr);
@@ -804,11 +1019,18 @@ static int admm_create(const AdmmConfig& cfg, int order, const int64_t* dims, co
   }
   TR_CUDA(cudaEventCreateWithFlags(&s->ev_main, cudaEventDisableTiming));
   cudaStream_t st = s->streams[0];
-  for (void* p : {(void*)s->l, (void*)s->lold, (void*)s->e, (void*)s->y, (void*)s->z})
+  // zero state (ghost faces included: the first sweep's right-hand side reads them)
+  auto zero = [&](T* p, bool ghost) -> int {
+    const int64_t f = ghost ? s->face : 0;
+    TR_CUDA(cudaMemsetAsync(p - f, 0, (N + 2 * f) * sizeof(T), st));
+    return 0;
+  };
+  if (zero(s->l, s->sharded) || zero(s->lold, s->sharded)) return 2;
+  for (void* p : {(void*)s->e, (void*)s->y, (void*)s->z})
     TR_CUDA(cudaMemsetAsync(p, 0, N * sizeof(T), st));
   for (int k = 0; k < nm; ++k) {
-    TR_CUDA(cudaMemsetAsync(s->gcur[k], 0, N * sizeof(T), st));
-    TR_CUDA(cudaMemsetAsync(s->lag[k], 0, N * sizeof(T), st));
+    if (zero(s->gcur[k], on_last(k)) || zero(s->lag[k], on_last(k))) return 2;
+    if (on_last(k) && (zero(s->gnew[k], true) || zero(s->lag2[k], true))) return 2;
   }
   // FFT twiddles and Laplacian eigenvalues of the gradient modes
   SolveSpec& ss = s->ss;
@@ -818,11 +1040,11 @@ static int admm_create(const AdmmConfig& cfg, int order, const int64_t* dims, co
   for (int i = 0; i < order; ++i) {
     ss.dims[i] = dims[i];
     ss.lam_off[i] = -1;
-    launch("setup", k_twiddles<T>, (unsigned)cdiv(dims[i], 256), 256, 0, st, (int)dims[i], s->tw[i]);
-    launch("setup", k_lap_eig, (unsigned)cdiv(dims[i], 256), 256, 0, st, (int)dims[i], s->lam + off);
+    launch("setup", k_twiddles<T>, (unsigned)cdiv(gd[i], 256), 256, 0, st, (int)gd[i], s->tw[i]);
+    launch("setup", k_lap_eig, (unsigned)cdiv(gd[i], 256), 256, 0, st, (int)gd[i], s->lam + off);
     for (int k = 0; k < nm; ++k)
       if (cfg.modes[k] == i) ss.lam_off[i] = off;
-    off += dims[i];
+    off += gd[i];
   }
   TR_LAUNCH_CHECK();
   TR_CUDA(cudaStreamSynchronize(st));

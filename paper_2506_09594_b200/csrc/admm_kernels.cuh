@@ -23,6 +23,11 @@ struct Geom {
   int64_t st[kMaxOrder];
   int64_t lst[kMaxOrder];  // st[a] / dims[0]: stride of axis a in the line index
   int64_t N;
+  // sharded last axis (multi-GPU): the arrays a stencil reads along axis
+  // `halo` carry one ghost face before and after their own faces, filled by the
+  // neighbouring ranks, so the circular neighbour of a boundary face is the
+  // ghost (no local wrap).  -1: every axis is whole and periodic.
+  int halo = -1;
 };
 
 // offsets of the previous / next element along axis a (a >= 1) for a line
@@ -30,6 +35,11 @@ struct Geom {
 __device__ __forceinline__ void axis_offsets(const Geom& g, int a, int64_t j, int64_t& prev,
                                              int64_t& next) {
   const int64_t n = g.dims[a], s = g.st[a];
+  if (a == g.halo) {
+    prev = -s;
+    next = s;
+    return;
+  }
   prev = j > 0 ? -s : s * (n - 1);
   next = j + 1 < n ? s : -s * (n - 1);
 }

@@ -51,6 +51,8 @@ struct SolveSpec {
   int d;                // tensor order
   int64_t dims[10];     // spectrum dims (axis 0 = n0/2+1 in the half-spectrum layout)
   int64_t lam_off[10];  // offset of axis k's 4 sin^2(pi j / n_k) table, -1 if k not in Gamma
+  int64_t lo_base = 0;  // global index of local lo-element 0 (the all-to-all layout of a
+                        // sharded solve: this rank's slice of the axes before the last)
 };
 
 // Stockham radix-4/2 FFT of the L lines in smem (element (l, k) at l*ls + k*ks),
@@ -334,7 +336,7 @@ __global__ void __launch_bounds__(256) k_fft_axis(const void* in, void* out,  //
       if (lo_lines) { l = e % L; k = e / L; } else { l = e / n; k = e % n; }
       const int64_t lo = lo_lines ? lo0 + l : 0;
       double den = 1.0;
-      int64_t rem = lo;
+      int64_t rem = ss.lo_base + lo;
       for (int a = 0; a < ss.d - 1; ++a) {
         const int64_t j = rem % ss.dims[a];
         rem /= ss.dims[a];
@@ -498,7 +500,7 @@ __global__ void __launch_bounds__(256) k_fft_axis_p(const void* in, void* out,  
         if (lo_lines) { l = e % L; k = e / L; } else { l = e / n; k = e % n; }
         const int64_t lo = lo_lines ? lo0 + l : 0;
         double den = 1.0;
-        int64_t rem = lo;
+        int64_t rem = ss.lo_base + lo;
         for (int a = 0; a < ss.d - 1; ++a) {
           const int64_t j = rem % ss.dims[a];
           rem /= ss.dims[a];
@@ -655,7 +657,7 @@ __global__ void __launch_bounds__(256) k_fft_p2(const void* in, void* out,  // m
     if (ss.active && threadIdx.x < L) {
       // per-line part of the denominator: axes 0..d-2 from the line's lo index
       double den = 1.0;
-      int64_t rem = lo0 + threadIdx.x;
+      int64_t rem = ss.lo_base + lo0 + threadIdx.x;
       for (int a = 0; a < ss.d - 1; ++a) {
         const int64_t j = rem % ss.dims[a];
         rem /= ss.dims[a];
@@ -1006,7 +1008,7 @@ __global__ void __launch_bounds__(256, 3) k_fft_t(const void* in, void* out,  //
     origin(t, lo0, hi0);
     if (ss.active && tid < L) {
       double den = 1.0;
-      int64_t rem = lo0 + tid;
+      int64_t rem = ss.lo_base + lo0 + tid;
       for (int a = 0; a < ss.d - 1; ++a) {
         const int64_t j = rem % ss.dims[a];
         rem /= ss.dims[a];

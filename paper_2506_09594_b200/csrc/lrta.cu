@@ -806,14 +806,15 @@ int tr_rsthosvd_bki(int dtype, const void* a, int order, const int64_t* dims,
                             workspace_bytes, st);
 }
 
-int tr_admm_create(int dtype, int order, const int64_t* dims, int kind, const void* obs_a,
+static int admm_create_any(int dtype, int order, const int64_t* dims, int kind, const void* obs_a,
                    const void* obs_b, const uint8_t* mask, int nmodes, const int64_t* modes,
                    int structure, int phi_kind, double phi_p0, double phi_p1, int psi_kind,
                    double psi_p0, double psi_p1, double lam, double lam2, double mu0,
                    double mu_max, double growth, double alpha, double mcount, int randomized,
                    const int64_t* ranks, const int64_t* blocks, const int64_t* krylov,
                    uint64_t seed, int transform_kind, const void* transform_mats,
-                   const double* alphas, void** handle) {
+                   const double* alphas, void** handle,
+                           const tr_comm* comm, int64_t last_all, int64_t last_off) {
   TR_REQUIRE(handle && dims && modes, "null pointer argument");
   TR_REQUIRE(kind >= 0 && kind <= 3, "bad solver kind %d", kind);
   TR_REQUIRE(structure >= 0 && structure <= 2, "bad shrink structure %d", structure);
@@ -856,11 +857,11 @@ int tr_admm_create(int dtype, int order, const int64_t* dims, int kind, const vo
   int rc;
   if (dtype == TR_F32) {
     Solver<float>* s = nullptr;
-    rc = admm_create<float>(cfg, order, dims, obs_a, obs_b, mask, &s);
+    rc = admm_create<float>(cfg, order, dims, obs_a, obs_b, mask, &s, comm, last_all, last_off);
     h->solver = s;
   } else {
     Solver<double>* s = nullptr;
-    rc = admm_create<double>(cfg, order, dims, obs_a, obs_b, mask, &s);
+    rc = admm_create<double>(cfg, order, dims, obs_a, obs_b, mask, &s, comm, last_all, last_off);
     h->solver = s;
   }
   if (rc) {
@@ -869,6 +870,36 @@ int tr_admm_create(int dtype, int order, const int64_t* dims, int kind, const vo
   }
   *handle = h;
   return 0;
+}
+
+int tr_admm_create(int dtype, int order, const int64_t* dims, int kind, const void* obs_a,
+                   const void* obs_b, const uint8_t* mask, int nmodes, const int64_t* modes,
+                   int structure, int phi_kind, double phi_p0, double phi_p1, int psi_kind,
+                   double psi_p0, double psi_p1, double lam, double lam2, double mu0,
+                   double mu_max, double growth, double alpha, double mcount, int randomized,
+                   const int64_t* ranks, const int64_t* blocks, const int64_t* krylov,
+                   uint64_t seed, int transform_kind, const void* transform_mats,
+                   const double* alphas, void** handle) {
+  return admm_create_any(dtype, order, dims, kind, obs_a, obs_b, mask, nmodes, modes, structure,
+                         phi_kind, phi_p0, phi_p1, psi_kind, psi_p0, psi_p1, lam, lam2, mu0,
+                         mu_max, growth, alpha, mcount, randomized, ranks, blocks, krylov, seed,
+                         transform_kind, transform_mats, alphas, handle, nullptr, 0, 0);
+}
+
+int tr_admm_create_sharded(int dtype, int order, const int64_t* dims, int kind,
+                           const void* obs_a, const uint8_t* mask, int nmodes,
+                           const int64_t* modes, int phi_kind, double phi_p0, double phi_p1,
+                           int psi_kind, double psi_p0, double psi_p1, double lam, double mu0,
+                           double mu_max, double growth, const int64_t* ranks,
+                           const int64_t* blocks, const int64_t* krylov, uint64_t seed,
+                           int64_t last_all, int64_t last_off, const tr_comm* comm,
+                           void** handle) {
+  TR_REQUIRE(comm, "null communicator");
+  TR_REQUIRE(kind == 0 || kind == 1, "the sharded solver runs GNRHTC (0) or GNHTC (1)");
+  return admm_create_any(dtype, order, dims, kind, obs_a, nullptr, mask, nmodes, modes, 0,
+                         phi_kind, phi_p0, phi_p1, psi_kind, psi_p0, psi_p1, lam, 0.0, mu0,
+                         mu_max, growth, 0.0, 0.0, 1, ranks, blocks, krylov, seed,
+                         TR_TRANSFORM_FFT, nullptr, nullptr, handle, comm, last_all, last_off);
 }
 
 int tr_admm_step(void* handle, double* out) {

@@ -1,5 +1,5 @@
-"""Multi-GPU randomized t-SVT: one rank per GPU, the tensor sharded along its
-last mode (row (e)).
+"""Multi-GPU randomized t-SVT and ADMM: one rank per GPU, the tensor sharded
+along its last mode (row (e)).
 
 For the reference algorithm -- Tucker compression of modes 0 and 1 by block
 Krylov sketching, then the transform-domain SVT of the r0 x r1 x faces core
@@ -30,7 +30,8 @@ from .sketch import SketchConfig, _resolve
 from .tensors import ColMajor, empty_like, from_device, to_device, workspace
 from .transform import DEFAULT_TRANSFORM, as_transform
 
-__all__ = ["shard_range", "allreduce_tensor", "DeviceAllreduce", "gnhtsvt_randomized_sharded"]
+__all__ = ["shard_range", "allreduce_tensor", "DeviceAllreduce", "gnhtsvt_randomized_sharded",
+           "DeviceComm", "gnrhtc_sharded", "gnhtc_sharded"]
 
 
 def shard_range(n: int, world: int, rank: int):
@@ -51,10 +52,10 @@ def allreduce_tensor(t, group=None):
 
 
 class _CudaArray:
-    """Zero-copy __cuda_array_interface__ view of fp64 device memory."""
+    """Zero-copy __cuda_array_interface__ view of device memory (fp64 or bytes)."""
 
-    def __init__(self, ptr: int, count: int):
-        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": "<f8",
+    def __init__(self, ptr: int, count: int, typestr: str = "<f8"):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": typestr,
                                          "data": (int(ptr), False), "version": 3,
                                          "stream": None}
 
@@ -138,3 +139,261 @@ def gnhtsvt_randomized_sharded(a_local, last_all: int, last_off: int,
         raise _lib.CudaPathError(f"all-reduce failed: {allreduce.error!r}")
     _lib.check(rc)
     return out if isinstance(a_local, ColMajor) else from_device(out)
+
+
+# -- the sharded ADMM (tr_admm_create_sharded) ---------------------------------
+
+class DeviceComm:
+    """The ``tr_comm`` collectives of the sharded ADMM over torch.distributed.
+
+    ``staged=False`` (NCCL): the callbacks wrap the device buffers without a
+    copy and issue the collective with the solver's stream as torch's current
+    stream -- stream-ordered, NVLink all-to-all / peer sends.  ``staged=True``
+    (any CPU backend, e.g. gloo; used to run several ranks on one test GPU):
+    each callback synchronises the stream, stages the bytes through host
+    memory, runs the collective there and copies the result back.
+    """
+
+    def __init__(self, group=None, staged=None):
+        import torch.distributed as dist
+
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.staged = (dist.get_backend(group) != "nccl") if staged is None else bool(staged)
+        self.error = None
+        self.calls = {"allreduce": 0, "alltoall": 0, "halo": 0}
+        self._fns = (_lib.COMM_ALLREDUCE_FN(self._allreduce), _lib.COMM_ALLTOALL_FN(self._alltoall),
+                     _lib.COMM_HALO_FN(self._halo))
+        self.struct = _lib.TrComm(self.world, self.rank, self._fns[0], self._fns[1], self._fns[2],
+                                  None)
+
+    # device views ---------------------------------------------------------
+    @staticmethod
+    def _view(ptr, count, typestr):
+        import torch
+
+        return torch.as_tensor(_CudaArray(ptr, count, typestr), device="cuda")
+
+    def _run(self, name, stream, body):
+        import torch
+
+        try:
+            with torch.cuda.stream(torch.cuda.ExternalStream(int(stream or 0))):
+                body()
+                if self.staged:
+                    torch.cuda.current_stream().synchronize()
+            self.calls[name] += 1
+            return 0
+        except Exception as exc:  # surfaced by the caller
+            self.error = exc
+            return 1
+
+    def _allreduce(self, buf, count, op, stream, user):
+        import torch.distributed as dist
+
+        def body():
+            t = self._view(ctypes.cast(buf, ctypes.c_void_p).value, count, "<f8")
+            red = dist.ReduceOp.MAX if op == 1 else dist.ReduceOp.SUM
+            if self.staged:
+                h = t.cpu()
+                dist.all_reduce(h, op=red, group=self.group)
+                t.copy_(h)
+            else:
+                dist.all_reduce(t, op=red, group=self.group)
+        return self._run("allreduce", stream, body)
+
+    def _alltoall(self, send, recv, nbytes, stream, user):
+        import torch.distributed as dist
+
+        def body():
+            n = int(nbytes) * self.world
+            s = self._view(send, n, "|u1")
+            r = self._view(recv, n, "|u1")
+            if self.staged:
+                hs = s.cpu()
+                hr = torch_empty_like_cpu(hs)
+                if self.world == 1:
+                    hr.copy_(hs)
+                else:
+                    dist.all_to_all_single(hr, hs, group=self.group)
+                r.copy_(hr)
+            else:
+                dist.all_to_all_single(r, s, group=self.group)
+        return self._run("alltoall", stream, body)
+
+    def _halo(self, first, last, gprev, gnext, nbytes, stream, user):
+        import torch.distributed as dist
+
+        def body():
+            n = int(nbytes)
+            W, r = self.world, self.rank
+            prev, nxt = (r - 1) % W, (r + 1) % W
+            f, l_ = self._view(first, n, "|u1"), self._view(last, n, "|u1")
+            gp, gn = self._view(gprev, n, "|u1"), self._view(gnext, n, "|u1")
+            if self.staged:
+                hf, hl = f.cpu(), l_.cpu()
+                hp, hn = torch_empty_like_cpu(hf), torch_empty_like_cpu(hf)
+                # my last face is the next rank's ghost_prev (tag 0), my first
+                # face the previous rank's ghost_next (tag 1)
+                reqs = [dist.isend(hl, _global(self.group, nxt), group=self.group, tag=0),
+                        dist.isend(hf, _global(self.group, prev), group=self.group, tag=1),
+                        dist.irecv(hp, _global(self.group, prev), group=self.group, tag=0),
+                        dist.irecv(hn, _global(self.group, nxt), group=self.group, tag=1)]
+                for q in reqs:
+                    q.wait()
+                gp.copy_(hp)
+                gn.copy_(hn)
+            else:
+                # same issue order on every rank: with two ranks prev == next,
+                # and NCCL pairs messages between two peers in issue order
+                ops = [dist.P2POp(dist.isend, l_, _global(self.group, nxt), self.group),
+                       dist.P2POp(dist.isend, f, _global(self.group, prev), self.group),
+                       dist.P2POp(dist.irecv, gp, _global(self.group, prev), self.group),
+                       dist.P2POp(dist.irecv, gn, _global(self.group, nxt), self.group)]
+                for q in dist.batch_isend_irecv(ops):
+                    q.wait()
+        return self._run("halo", stream, body)
+
+
+def torch_empty_like_cpu(t):
+    import torch
+
+    return torch.empty_like(t, device="cpu")
+
+
+def _global(group, rank):
+    import torch.distributed as dist
+
+    return rank if group is None else dist.get_global_rank(group, rank)
+
+
+class ShardedSolver:
+    """One sharded GNRHTC / GNHTC run (tr_admm_create_sharded) on this rank's slab."""
+
+    def __init__(self, kind, cm: ColMajor, mask_dev, cfg, modes, lam, last_all, last_off,
+                 comm: DeviceComm):
+        self.lib = _lib.lib()
+        self.cm = cm
+        self.comm = comm
+        self.keep = [cm, mask_dev]
+        dims = cm.dims
+        gdims = tuple(dims[:-1]) + (int(last_all),)
+        sk = cfg.sketch
+        sk, ranks, blocks, krylov = _resolve(sk, gdims)
+        phi = encode_penalty(cfg.phi)
+        psi = encode_penalty(cfg.psi)
+        handle = ctypes.c_void_p()
+        rc = self.lib.tr_admm_create_sharded(
+            cm.dtype_code, len(dims), _lib.i64(dims), 0 if kind == "gnrhtc" else 1,
+            ctypes.c_void_p(cm.ptr), ctypes.c_void_p(mask_dev.data_ptr()), len(modes),
+            _lib.i64(modes), phi[0], phi[1], phi[2], psi[0], psi[1], psi[2], float(lam),
+            float(cfg.mu0), float(cfg.mu_max), float(cfg.growth), _lib.i64(ranks),
+            _lib.i64(blocks), _lib.i64(krylov), ctypes.c_uint64(int(sk.seed) & (2 ** 64 - 1)),
+            int(last_all), int(last_off), ctypes.byref(comm.struct), ctypes.byref(handle))
+        self._check(rc)
+        self.handle = handle
+        self.out = (ctypes.c_double * 15)()
+
+    def _check(self, rc):
+        if rc and self.comm.error is not None:
+            raise _lib.CudaPathError(f"collective failed: {self.comm.error!r}")
+        _lib.check(rc)
+
+    def step(self):
+        self._check(self.lib.tr_admm_step(self.handle, self.out))
+        return list(self.out)
+
+    def read(self, which: int) -> ColMajor:
+        import torch
+
+        flat = torch.empty_like(self.cm.flat)
+        _lib.check(self.lib.tr_admm_read(self.handle, which, ctypes.c_void_p(flat.data_ptr()),
+                                         _lib.stream_ptr()))
+        return ColMajor(flat, self.cm.dims, self.cm.kind, self.cm.np_dtype)
+
+    def stream(self):
+        return self.lib.tr_admm_stream(self.handle)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.tr_admm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _sharded_complete(mobs_local, mask_local, cfg, last_all, last_off, comm, group, noise_free):
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    from .solvers import SolveReport
+    from .tensors import mask_to_device
+
+    t0 = time.perf_counter()
+    cfg.validate()
+    if not cfg.randomized:
+        raise ValueError("the sharded solver needs randomized=True with a SketchConfig")
+    if cfg.pure_lowrank:
+        raise ValueError("the sharded solver runs the gradient chain (pure_lowrank=False)")
+    if str(cfg.structure).lower() != "entry":
+        raise ValueError("the sharded solver supports structure='entry'")
+    comm = DeviceComm(group) if comm is None else comm
+    cm = mobs_local if isinstance(mobs_local, ColMajor) else to_device(mobs_local)
+    dims = cm.dims
+    if tuple(mask_local.shape) != dims:
+        raise ValueError("mask shape must match the observation tensor")
+    mdev = mask_to_device(mask_local)
+    gdims = tuple(dims[:-1]) + (int(last_all),)
+    lam = cfg.lam_for(gdims)
+    modes = cfg.device_modes(gdims)
+    run = ShardedSolver("gnhtc" if noise_free else "gnrhtc", cm, mdev, cfg, modes, lam, last_all,
+                        last_off, comm)
+    report = SolveReport()
+    try:
+        for _ in range(cfg.max_iters):
+            o = run.step()
+            report.residual_history.append(o[0:5])
+            report.diff_fro_history.append([o[5], o[6], o[7]])
+            report.feas_fro_history.append([o[8], o[9]])
+            report.multiplier_history.append([o[10], o[11]])
+            report.mu_history.append(o[12])
+            report.iterations += 1
+            if max(o[0:5]) <= cfg.tol and max(o[5:8]) <= cfg.tol:
+                report.converged = True
+                break
+        l_cm = run.read(0)
+        e_cm = run.read(1)
+    finally:
+        run.close()
+    fin = torch.tensor([float(torch.isfinite(l_cm.flat).all())], dtype=torch.float64)
+    if comm.world > 1:
+        dist.all_reduce(fin, op=dist.ReduceOp.MIN, group=group)
+    if fin.item() < 1.0:
+        raise FloatingPointError("solver produced non-finite iterates")
+    report.objective = {"lambda": lam}
+    report.wall_clock = time.perf_counter() - t0
+    return from_device(l_cm), from_device(e_cm), report
+
+
+def gnrhtc_sharded(mobs_local, mask_local, cfg, last_all: int, last_off: int, comm=None,
+                   group=None):
+    """Robust completion of a tensor sharded along its last mode over the ranks
+    of ``group`` (one GPU each).  Every rank passes its slab of faces
+    ``[last_off, last_off + mobs_local.shape[-1])``; the residual history is
+    global.  Returns this rank's ``(L, E, report)`` slabs."""
+    return _sharded_complete(mobs_local, mask_local, cfg, last_all, last_off, comm, group, False)
+
+
+def gnhtc_sharded(mobs_local, mask_local, cfg, last_all: int, last_off: int, comm=None,
+                  group=None):
+    """Noise-free completion, sharded like :func:`gnrhtc_sharded`: ``(L, report)``."""
+    l, _, report = _sharded_complete(mobs_local, mask_local, cfg, last_all, last_off, comm, group,
+                                     True)
+    return l, report
