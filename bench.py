@@ -2,7 +2,7 @@
 """Benchmark of the B200 randomized t-SVT / ADMM hot path ("Measurement").
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--step admm|lrta|tsvt-sharded]
+                    [--step admm|lrta|tsvt-sharded|admm-sharded] [--lrta bki|blbp]
 
 Workload (BASELINE.json configs[1]): order-3 robust tensor PCA, 1024x1024x128
 float32, tubal rank 20 from Gaussian factors (unit RMS), 10% sparse outliers
@@ -17,7 +17,10 @@ randomized t-SVT voxels/s = 3 x 1024*1024*128 x sweeps/s (whole job); ADMM
 sweeps/s is reported beside it.  ``--step lrta`` times a single t-SVT;
 ``--step tsvt-sharded`` times one t-SVT of the whole tensor sharded along its
 last mode over the N ranks (strong scaling, NCCL all-reduces of the Krylov
-blocks / Ritz Gram / core, shard.py).  Every
+blocks / Ritz Gram / core, shard.py); ``--step admm-sharded`` times one GNRHTC
+sweep of BASELINE configs[4]'s tensor sharded along its last mode (global
+2048x2048x32x(4N), 4 faces per rank: exactly configs[4] at N = 8; weak
+scaling; all-to-all FFT transpose, halo exchanges, sharded t-SVTs).  Every
 tensor is 512 MB (> 126 MB L2), so no explicit flush is needed.
 
 Multi-GPU: one process per GPU (torchrun); each rank solves its own problem
@@ -777,13 +780,158 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+CONFIG4 = {
+    "workload": "robust-completion-2048x2048x32x(4N)-f32",
+    "local_dims": (2048, 2048, 32, 4),
+    "tubal_rank": 30,
+    "observed": 0.20,
+    "outlier_frac": 0.05,
+    "outlier_amp": 5.0,
+    "ranks": (40, 40),
+    "blocks": (10, 10),
+    "krylov": (3, 3),
+}
+
+
+def make_config4_slab(torch, world, rank, seed=4321):
+    """This rank's slab of BASELINE configs[4]'s tensor at world size N: global
+    dims (2048, 2048, 32, 4N) -- exactly configs[4] at N = 8 -- as
+    sum_{r<30} a_r(i0) b_r(i1) c_r(i2, i3) with Gaussian factors (tubal rank <= 30),
+    unit RMS, 5% outliers U[-5, 5], 20% observed.  Every rank draws the shared
+    factors from the same seed and slices c along the last mode, so the slabs
+    tile one global tensor.  Setup only (outside every timed region)."""
+    n0, n1, n2, nl = CONFIG4["local_dims"]
+    r = CONFIG4["tubal_rank"]
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    a = torch.randn((n0, r), generator=g, device="cuda")
+    b = torch.randn((n1, r), generator=g, device="cuda")
+    c = torch.randn((n2, nl * world, r), generator=g, device="cuda")[:, rank * nl:(rank + 1) * nl]
+    # column-major flat (i0 fastest): x[i3, i2, i1, i0] in C order
+    x = torch.einsum("ir,jr,klr->lkji", a, b, c).contiguous() / math.sqrt(r)
+    flat = x.reshape(-1)
+    gl = torch.Generator(device="cuda").manual_seed(seed + 1 + rank)
+    out = torch.rand(flat.numel(), generator=gl, device="cuda") < CONFIG4["outlier_frac"]
+    amp = CONFIG4["outlier_amp"]
+    flat = torch.where(out, (torch.rand(flat.numel(), generator=gl, device="cuda") * 2 - 1) * amp,
+                       flat)
+    mask = (torch.rand(flat.numel(), generator=gl, device="cuda") < CONFIG4["observed"])
+    flat = torch.where(mask, flat, torch.zeros_like(flat))
+    return flat.contiguous(), mask.to(torch.uint8)
+
+
+def run_admm_sharded(args):
+    """One GNRHTC sweep of configs[4] sharded along the last mode over the N
+    ranks (tr_admm_create_sharded; weak scaling, 4 faces per rank)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2506_09594_b200 as pk
+    from paper_2506_09594_b200 import _lib
+    from paper_2506_09594_b200.shard import DeviceComm, ShardedSolver
+    from paper_2506_09594_b200.tensors import ColMajor
+
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        import socket
+
+        with socket.socket() as sock:
+            sock.bind(("127.0.0.1", 0))
+            port = sock.getsockname()[1]
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                                world_size=1, device_id=torch.device("cuda", local))
+    lib = _lib.lib()
+    ldims = CONFIG4["local_dims"]
+    gdims = ldims[:-1] + (ldims[-1] * world,)
+    Nl = math.prod(ldims)
+    flat, mask = make_config4_slab(torch, world, rank)
+    cm = ColMajor(flat, ldims, "torch", None)
+    sk = pk.SketchConfig(mode="fixed-rank", order=(0, 1), ranks=CONFIG4["ranks"],
+                         blocks=CONFIG4["blocks"], krylov=CONFIG4["krylov"], seed=7)
+    cfg = pk.SolverConfig(phi=pk.MCP(2.5), psi=pk.MCP(2.5), randomized=True, sketch=sk,
+                          max_iters=args.steps + args.warmup, tol=1e-30)
+    comm = DeviceComm()
+    modes = tuple(range(len(ldims)))
+    run = ShardedSolver("gnrhtc", cm, mask, cfg, modes, cfg.lam_for(gdims), gdims[-1],
+                        rank * ldims[-1], comm)
+    stream = torch.cuda.ExternalStream(run.stream())
+    for _ in range(args.warmup):
+        run.step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = lib.tr_launch_count()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            run.step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = lib.tr_launch_count() - launches0
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    run.close()
+    ms_per_step = ms / args.steps
+    value = len(modes) * Nl * world * args.steps / (ms / 1e3)
+    # end to end through the public API, host slabs in / out
+    host = flat.reshape(tuple(reversed(ldims))).permute(3, 2, 1, 0).cpu().numpy()
+    host_mask = mask.reshape(tuple(reversed(ldims))).permute(3, 2, 1, 0).cpu().numpy().astype(bool)
+    del flat, mask, cm
+    torch.cuda.empty_cache()
+    e2e_iters = 3
+    cfg_e = pk.SolverConfig(phi=pk.MCP(2.5), psi=pk.MCP(2.5), randomized=True, sketch=sk,
+                            max_iters=e2e_iters, tol=1e-30)
+    dist.barrier()
+    t0 = time.perf_counter()
+    l_h, e_h, rep = pk.gnrhtc_sharded(host, host_mask, cfg_e, gdims[-1], rank * ldims[-1], comm)
+    e2e_s = time.perf_counter() - t0
+    t = torch.tensor([e2e_s], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_s = float(t.item())
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded Gaussian CP factors, tubal rank <= 30, 5% outliers "
+                    "U[-5, 5], 20% observed)",
+            "config": {"workload": CONFIG4["workload"], "step": "admm-sharded",
+                       "global_dims": list(gdims), "local_dims": list(ldims),
+                       "ranks": list(CONFIG4["ranks"]), "blocks": list(CONFIG4["blocks"]),
+                       "krylov": list(CONFIG4["krylov"]), "gradient_modes": list(modes),
+                       "parallelism": f"last-mode-shard{world}",
+                       "note": "BASELINE configs[4] (2048x2048x32x32) at N = 8",
+                       "l2": "every local tensor 2.1 GB > 126 MB L2 (no flush needed)"},
+            "admm_iters_per_s": 1e3 / ms_per_step,
+            "e2e": {"value": len(modes) * Nl * world * rep.iterations / e2e_s, "unit": UNIT,
+                    "h2d_bytes_per_step": (host.nbytes + host_mask.nbytes) / rep.iterations,
+                    "d2h_bytes_per_step": (l_h.nbytes + e_h.nbytes) / rep.iterations,
+                    "per_rank_bytes": True,
+                    "api": f"paper_2506_09594_b200.gnrhtc_sharded(numpy slab, "
+                           f"max_iters={rep.iterations})"},
+            "gpu_launches": launches, "clocks": clk.summary(),
+            "collective_calls": dict(comm.calls),
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--step", choices=("admm", "lrta", "tsvt-sharded"), default="admm")
+    ap.add_argument("--step", choices=("admm", "lrta", "tsvt-sharded", "admm-sharded"),
+                    default="admm")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-legs", action="store_true", help="skip the fp64 and BLBP legs")
     ap.add_argument("--lrta", choices=("bki", "blbp"), default="bki",
@@ -792,6 +940,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.step == "admm-sharded":
+        run_admm_sharded(args)
     else:
         run_ours(args)
 

@@ -220,6 +220,27 @@ static void fft_pass_p2(int mode, const void* in, void* dst, double scale, int64
   }
 }
 
+// k_fft_reg for a short power-of-two axis with a wide lo stride; false otherwise
+template <typename T>
+static bool fft_reg(const cpx<T>* tw, const double* lam, void* data, int n, int64_t stv,
+                    int64_t hi, int inverse, const SolveSpec& ss, cudaStream_t st) {
+  static const bool off = getenv("TR_NO_FFT_REG") != nullptr;
+  if (off || stv < 32 || n > 32 || n < 2 || (n & (n - 1)) != 0) return false;
+  const unsigned grid = (unsigned)std::max<int64_t>(
+      1, std::min<int64_t>(cdiv(stv * hi, 256), 16ll * num_sms()));
+  cpx<T>* d = (cpx<T>*)data;
+#define TR_FR(NN) launch("fft", k_fft_reg<T, NN>, grid, 256, 0, st, d, stv, hi, tw, inverse, ss, lam)
+  switch (n) {
+    case 2: TR_FR(2); break;
+    case 4: TR_FR(4); break;
+    case 8: TR_FR(8); break;
+    case 16: TR_FR(16); break;
+    default: TR_FR(32); break;
+  }
+#undef TR_FR
+  return true;
+}
+
 // forward FFT over all axes, diagonal solve in the last-axis pass, inverse FFT
 template <typename T>
 static int fft_solve(Solver<T>& s, const T* rhs, T* out, cudaStream_t st) {
@@ -238,6 +259,9 @@ static int fft_solve(Solver<T>& s, const T* rhs, T* out, cudaStream_t st) {
     const int64_t stv = mode == FFT_C2C ? sg.st[a] : 1;
     const int64_t hi = mode == FFT_C2C ? sg.N / (stv * n) : g.N / n;
     const bool pow2 = (nt & (nt - 1)) == 0;
+    if (mode == FFT_C2C && in == dst &&
+        fft_reg<T>((const cpx<T>*)s.tw[a], s.lam, dst, n, stv, hi, inverse, ss, st))
+      return 0;
     // persistent double-buffered kernel: pow2, <= 2048-point tiles, 16B-aligned real lines
     const bool persistent = pow2 && nt >= 8 && nt <= 2048 &&
                             (mode != FFT_R2C || (n * (int64_t)sizeof(T)) % 16 == 0) &&
@@ -292,6 +316,7 @@ static int fft_solve(Solver<T>& s, const T* rhs, T* out, cudaStream_t st) {
 template <typename T>
 static int fft_c2c(const cpx<T>* tw, const double* lam, void* data, int n, int64_t stv, int64_t hi,
                    int inverse, const SolveSpec& ss, cudaStream_t st) {
+  if (fft_reg<T>(tw, lam, data, n, stv, hi, inverse, ss, st)) return 0;
   const bool pow2 = (n & (n - 1)) == 0;
   if (pow2 && n >= 8 && n <= 2048 && getenv("TR_FFT_SIMPLE") == nullptr) {
     fft_pass_p2<T>(FFT_C2C, data, data, 1.0, stv, n, hi, tw, inverse, ss, lam, 0, st);

@@ -36,6 +36,45 @@ __device__ __forceinline__ cpx<T> cmulc(cpx<T> a, cpx<T> b) {
 template <typename T>
 __device__ __forceinline__ cpx<T> cconjt(cpx<T> a) { return {a.re, -a.im}; }
 
+__host__ __device__ constexpr int bitrev_c(int i, int bits) {
+  return bits == 0 ? 0 : (((i & 1) << (bits - 1)) | bitrev_c(i >> 1, bits - 1));
+}
+
+template <int N>
+__host__ __device__ constexpr int log2_c() {
+  return N <= 1 ? 0 : 1 + log2_c<N / 2>();
+}
+
+// In-register radix-2 FFT of N = 2^k points (unnormalised; ts = the N-point
+// forward table, conjugated for the inverse).
+template <typename T, int N>
+__device__ __forceinline__ void reg_fft(cpx<T> (&v)[N], const cpx<T>* ts, bool inverse) {
+  constexpr int LB = log2_c<N>();
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const int j = bitrev_c(i, LB);
+    if (j > i) {
+      const cpx<T> t = v[i];
+      v[i] = v[j];
+      v[j] = t;
+    }
+  }
+#pragma unroll
+  for (int len = 2; len <= N; len <<= 1) {
+#pragma unroll
+    for (int i = 0; i < N; i += len)
+#pragma unroll
+      for (int j = 0; j < len / 2; ++j) {
+        cpx<T> w = ts[j * (N / len)];
+        if (inverse) w.im = -w.im;
+        const cpx<T> u = v[i + j];
+        const cpx<T> t = cmulc(w, v[i + j + len / 2]);
+        v[i + j] = cadd(u, t);
+        v[i + j + len / 2] = csub(u, t);
+      }
+  }
+}
+
 // tw[k] = exp(-2 pi i k / n), k < n, computed in fp64 with exact argument reduction
 template <typename T>
 __global__ void k_twiddles(int n, cpx<T>* __restrict__ tw) {
@@ -54,6 +93,54 @@ struct SolveSpec {
   int64_t lo_base = 0;  // global index of local lo-element 0 (the all-to-all layout of a
                         // sharded solve: this rank's slice of the axes before the last)
 };
+
+// C2C pass along a short power-of-two axis (N <= 32) with lo-stride st >= 32,
+// in place: one thread per line, the whole line in registers, every load and
+// store a coalesced warp access (consecutive threads = consecutive lo).  No
+// shared-memory tile or barrier -- the tile kernels below spend most of their
+// issue slots on those for short axes.  `ss.active`: forward, divide,
+// inverse (the solve along the last axis).
+template <typename T, int N>
+__global__ void __launch_bounds__(256) k_fft_reg(cpx<T>* __restrict__ data, int64_t st,
+                                                 int64_t hi, const cpx<T>* __restrict__ tw,
+                                                 int inverse, SolveSpec ss,
+                                                 const double* __restrict__ lam) {
+  __shared__ cpx<T> ts[N];
+  __shared__ double lamk[N];
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    ts[k] = tw[k];
+    lamk[k] = (ss.active && ss.lam_off[ss.d - 1] >= 0) ? lam[ss.lam_off[ss.d - 1] + k] : 0.0;
+  }
+  __syncthreads();
+  const int64_t total = st * hi;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lo = e % st, h = e / st;
+    cpx<T>* p = data + lo + st * (int64_t)N * h;
+    cpx<T> v[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) v[k] = p[st * k];
+    reg_fft<T, N>(v, ts, ss.active ? false : inverse != 0);
+    if (ss.active) {
+      double den = 1.0;
+      int64_t rem = ss.lo_base + lo;
+      for (int a = 0; a < ss.d - 1; ++a) {
+        const int64_t j = rem % ss.dims[a];
+        rem /= ss.dims[a];
+        if (ss.lam_off[a] >= 0) den += lam[ss.lam_off[a] + j];
+      }
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const T inv = (T)(1.0 / (den + lamk[k]));
+        v[k].re *= inv;
+        v[k].im *= inv;
+      }
+      reg_fft<T, N>(v, ts, true);
+    }
+#pragma unroll
+    for (int k = 0; k < N; ++k) p[st * k] = v[k];
+  }
+}
 
 // Stockham radix-4/2 FFT of the L lines in smem (element (l, k) at l*ls + k*ks),
 // in place: every stage reads all groups into registers, syncs, writes.
@@ -253,6 +340,7 @@ __device__ __forceinline__ void lines_fft(cpx<T>* buf, cpx<T>* tmp, int L, int n
 
 // Pass modes
 enum FftMode { FFT_C2C = 0, FFT_R2C = 1, FFT_C2R = 2 };
+
 
 // One pass along an axis.
 //  C2C: complex in/out, axis length n (lo-stride st, hi lines).

@@ -327,10 +327,13 @@ struct TsqrPlan {
   size_t sm_local, sm_top, sm_form;
 };
 
-static TsqrPlan tsqr_plan(int64_t m, int s) {
+static TsqrPlan tsqr_plan(int64_t m, int s, bool wide = false) {
   TsqrPlan p{};
   const int64_t cap = 200 * 1024;
-  int64_t rb = std::min<int64_t>(256, (cap / 8 / s - 1) / 2);
+  // row blocks of <= 256 rows; `wide`: as many rows as the form stage holds,
+  // so fewer blocks -- a shorter R stack for the single-CTA top stage
+  int64_t rb = (cap / 8 - s) / (2 * s) - 1;  // largest RB whose form stage fits
+  if (!wide) rb = std::min<int64_t>(256, rb);
   rb = std::max<int64_t>(rb, s);
   p.RB = (int)rb;
   p.nb = (int)cdiv(m, rb);
@@ -356,7 +359,8 @@ static void orth_basis(int64_t m, int s, Bufs<T>& bf, int64_t* info, cudaStream_
            bf.Z, bf.Zt, info);
     return;
   }
-  const TsqrPlan p = tsqr_plan(m, s);
+  TsqrPlan p = tsqr_plan(m, s);
+  if (!p.ok) p = tsqr_plan(m, s, true);
   if (!p.ok) {
     launch("orth", k_orth<T>, 1, 1024, 0, st, bf.K, m, s, bf.work, bf.Z, bf.Zt, info);
     return;
@@ -416,17 +420,17 @@ static bool tmap_f32(CUtensorMap* map, const float* base, int64_t rows, int64_t 
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// W = A^T Z on the tensor cores (proj_tc.cuh) when the unfolding suits it
+// W = A^T Z on the tensor cores (proj_tc.cuh) when the unfolding suits it:
+// s <= 32 in one pass with the fused Gram; 32 < s <= 64 as two column blocks
+// of W (two passes over A) and the Gram from W afterwards.
 static bool project(const float* A, int64_t m, int64_t n, int s, Bufs<float>& bf, cudaStream_t st) {
-  if (m % 32 != 0 || s > 32 || ((uintptr_t)A % 16) != 0 || n >= (1ll << 31) ||
+  if (m % 32 != 0 || s > 64 || ((uintptr_t)A % 16) != 0 || n >= (1ll << 31) ||
       getenv("TR_NO_TC") != nullptr)
     return false;
   CUtensorMap ma, mh, ml;
   if (!tmap_f32(&ma, A, m, n, 128) || !tmap_f32(&mh, bf.zhi, m, 32, 32) ||
       !tmap_f32(&ml, bf.zlo, m, 32, 32))
     return false;
-  launch("proj_split", k_split_z, (unsigned)cdiv(m * 32, 256), 256, 0, st, bf.Z, m, s, bf.zhi,
-         bf.zlo);
   const int64_t ntiles = cdiv(n, 128);
   const int64_t grid = std::min<int64_t>(ntiles, stream_sms());
   const size_t smem = (size_t)kPwSmemBytes + 1024;
@@ -435,9 +439,23 @@ static bool project(const float* A, int64_t m, int64_t n, int s, Bufs<float>& bf
     cudaFuncSetAttribute(k_proj_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  launch("proj_tc", k_proj_ws, (unsigned)grid, kPwThreads, smem, st, ma, mh, ml, m, n, s, bf.W,
-         bf.Mpart);
-  reduce(bf.Mpart, grid, (int64_t)s * s, bf.M, st);
+  for (int j0 = 0; j0 < s; j0 += 32) {
+    const int cnt = std::min(32, s - j0);
+    launch("proj_split", k_split_z, (unsigned)cdiv(m * 32, 256), 256, 0, st,
+           (const double*)(bf.Z + m * (int64_t)j0), m, cnt, bf.zhi, bf.zlo);
+    launch("proj_tc", k_proj_ws, (unsigned)grid, kPwThreads, smem, st, ma, mh, ml, m, n, cnt,
+           bf.W + j0, s <= 32 ? bf.Mpart : (double*)nullptr, s);
+  }
+  if (s <= 32) {
+    reduce(bf.Mpart, grid, (int64_t)s * s, bf.M, st);
+  } else {
+    const int64_t mparts = std::min<int64_t>(cdiv(n, 64), bf.max_mparts);
+    const int64_t rpb = cdiv(n, mparts);
+    const int64_t mp = cdiv(n, rpb);
+    launch("wtw", k_wtw<float>, (unsigned)mp, 256, 32 * s * sizeof(double), st, (const float*)bf.W,
+           n, s, rpb, bf.Mpart);
+    reduce(bf.Mpart, mp, (int64_t)s * s, bf.M, st);
+  }
   return true;
 }
 

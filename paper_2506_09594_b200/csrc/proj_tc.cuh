@@ -114,13 +114,13 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// W (n x s row-major) = A^T Z and part[blk] = this CTA's share of W^T W (s x s,
-// fp64).  A: m x n column-major (tensor map mapA, box 32 x 128); Z_hi / Z_lo:
+// W (n x s, row stride ldw) = A^T Z and part[blk] = this CTA's share of W^T W
+// (s x s, fp64; part == nullptr: W only).  A: m x n column-major (tensor map mapA, box 32 x 128); Z_hi / Z_lo:
 // m x 32 column-major (maps, box 32 x 32).  m % 32 == 0.
 __global__ void __launch_bounds__(kPwThreads, 1)
     k_proj_ws(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapZh,
               const __grid_constant__ CUtensorMap mapZl, int64_t m, int64_t n, int s,
-              float* __restrict__ W, double* __restrict__ part) {
+              float* __restrict__ W, double* __restrict__ part, int ldw) {
   extern __shared__ __align__(1024) unsigned char pw_raw[];
   __shared__ __align__(8) uint64_t full[kPwStages], empty[kPwStages];
   __shared__ __align__(8) uint64_t lo_ready[kPwLo], lo_empty[kPwLo];
@@ -253,11 +253,12 @@ __global__ void __launch_bounds__(kPwThreads, 1)
       mbar_arrive(&tempty[acc]);
       const int64_t col = (blockIdx.x + t * gridDim.x) * 128 + row;
       if (col < n) {
-        float* dst = W + col * s;
+        float* dst = W + col * ldw;
 #pragma unroll
         for (int j = 0; j < 32; ++j)
           if (j < s) dst[j] = w[j];
       }
+      if (part == nullptr) continue;  // column block of a wider W: Gram formed afterwards
       asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile's Gram reads done
 #pragma unroll
       for (int j = 0; j < 32; ++j) wt[row][j] = col < n ? w[j] : 0.f;
@@ -273,7 +274,7 @@ __global__ void __launch_bounds__(kPwThreads, 1)
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int e = et + 128 * u, j = e >> 5, k = e & 31;
-      if (j < s && k < s) part[(int64_t)blockIdx.x * s * s + j * s + k] = g[u];
+      if (part != nullptr && j < s && k < s) part[(int64_t)blockIdx.x * s * s + j * s + k] = g[u];
     }
   }
   tc_fence_before();
