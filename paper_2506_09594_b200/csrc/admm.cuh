@@ -313,10 +313,60 @@ static int fft_solve(Solver<T>& s, const T* rhs, T* out, cudaStream_t st) {
 
 // One C2C pass along a spectrum axis of length n (lo-stride stv, hi lines of
 // lines); persistent power-of-two kernel when possible, generic otherwise.
+// k_fft4 (four-step register FFT) for 256..1024-point contiguous lines or
+// 128..256-point strided lines; false otherwise
+template <typename T, int P, int N2, bool STRIDED, int MINB>
+static void fft4_launch(const cpx<T>* tw, const double* lam, void* data, int64_t stv, int64_t hi,
+                        int inverse, const SolveSpec& ss, cudaStream_t st) {
+  const size_t smem = (size_t)fft4_smem_cpx<N2>() * sizeof(cpx<T>);
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    cudaFuncSetAttribute(k_fft4<T, P, N2, STRIDED, MINB>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fft4<T, P, N2, STRIDED, MINB>, 256,
+                                                  smem);
+    per_sm = std::max(per_sm, 1);
+  }
+  const int64_t nlines = STRIDED ? stv * hi : hi;
+  const int64_t ntiles = cdiv(nlines, 256 / P);
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)per_sm * num_sms());
+  launch("fft", k_fft4<T, P, N2, STRIDED, MINB>, grid, 256, smem, st, (cpx<T>*)data, stv, hi, tw,
+         inverse, ss, lam);
+}
+
+template <typename T>
+static bool fft4(const cpx<T>* tw, const double* lam, void* data, int n, int64_t stv, int64_t hi,
+                 int inverse, const SolveSpec& ss, cudaStream_t st) {
+  static const bool off = getenv("TR_NO_FFT4") != nullptr;
+  static const int mb = getenv("TR_FFT4_MINB") ? atoi(getenv("TR_FFT4_MINB")) : 2;
+  if (off) return false;
+  if (stv == 1 && !ss.active) {
+    switch (n) {
+      case 256: fft4_launch<T, 16, 16, false, 2>(tw, lam, data, stv, hi, inverse, ss, st); return true;
+      case 512: fft4_launch<T, 16, 32, false, 1>(tw, lam, data, stv, hi, inverse, ss, st); return true;
+      case 1024:
+        if (mb == 2) fft4_launch<T, 32, 32, false, 2>(tw, lam, data, stv, hi, inverse, ss, st);
+        else fft4_launch<T, 32, 32, false, 1>(tw, lam, data, stv, hi, inverse, ss, st);
+        return true;
+      default: return false;
+    }
+  }
+  if (stv >= 32) {
+    switch (n) {
+      case 64: fft4_launch<T, 4, 16, true, 2>(tw, lam, data, stv, hi, inverse, ss, st); return true;
+      case 128: fft4_launch<T, 8, 16, true, 2>(tw, lam, data, stv, hi, inverse, ss, st); return true;
+      case 256: fft4_launch<T, 8, 32, true, 1>(tw, lam, data, stv, hi, inverse, ss, st); return true;
+      default: return false;
+    }
+  }
+  return false;
+}
+
 template <typename T>
 static int fft_c2c(const cpx<T>* tw, const double* lam, void* data, int n, int64_t stv, int64_t hi,
                    int inverse, const SolveSpec& ss, cudaStream_t st) {
   if (fft_reg<T>(tw, lam, data, n, stv, hi, inverse, ss, st)) return 0;
+  if (fft4<T>(tw, lam, data, n, stv, hi, inverse, ss, st)) return 0;
   const bool pow2 = (n & (n - 1)) == 0;
   if (pow2 && n >= 8 && n <= 2048 && getenv("TR_FFT_SIMPLE") == nullptr) {
     fft_pass_p2<T>(FFT_C2C, data, data, 1.0, stv, n, hi, tw, inverse, ss, lam, 0, st);

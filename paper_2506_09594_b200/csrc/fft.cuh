@@ -45,34 +45,52 @@ __host__ __device__ constexpr int log2_c() {
   return N <= 1 ? 0 : 1 + log2_c<N / 2>();
 }
 
+// One radix-2 stage (butterfly span LEN) of reg_fft, fully unrolled.
+template <typename T, int N, int TS, int LEN>
+__device__ __forceinline__ void reg_fft_stage(cpx<T> (&v)[N], const cpx<T>* ts, bool inverse) {
+#pragma unroll
+  for (int i = 0; i < N; i += LEN)
+#pragma unroll
+    for (int j = 0; j < LEN / 2; ++j) {
+      constexpr int STEP = N / LEN;
+      const int widx = j * STEP;  // of N
+      const cpx<T> u = v[i + j];
+      const cpx<T> x = v[i + j + LEN / 2];
+      cpx<T> t;
+      if (widx == 0) {
+        t = x;
+      } else if (4 * widx == N) {  // w = -i (forward) / +i (inverse)
+        t = inverse ? cpx<T>{-x.im, x.re} : cpx<T>{x.im, -x.re};
+      } else {
+        cpx<T> w = ts[widx * TS];
+        if (inverse) w.im = -w.im;
+        t = cmulc(w, x);
+      }
+      v[i + j] = cadd(u, t);
+      v[i + j + LEN / 2] = csub(u, t);
+    }
+  if constexpr (LEN < N) reg_fft_stage<T, N, TS, 2 * LEN>(v, ts, inverse);
+}
+
 // In-register radix-2 FFT of N = 2^k points (unnormalised; ts = the N-point
-// forward table, conjugated for the inverse).
-template <typename T, int N>
+// forward table -- or any table of which every TS-th entry is, TS = 1 by
+// default -- conjugated for the inverse).  Every index is a compile-time
+// constant (stages unrolled by template recursion), so the line stays in
+// registers and the trivial twiddles (1, -i) cost nothing.
+template <typename T, int N, int TS = 1>
 __device__ __forceinline__ void reg_fft(cpx<T> (&v)[N], const cpx<T>* ts, bool inverse) {
   constexpr int LB = log2_c<N>();
 #pragma unroll
   for (int i = 0; i < N; ++i) {
-    const int j = bitrev_c(i, LB);
+    // bit reversal as a bit-reverse intrinsic of a constant (folded after unrolling)
+    const int j = LB == 0 ? 0 : (int)(__brev((unsigned)i) >> (32 - LB));
     if (j > i) {
       const cpx<T> t = v[i];
       v[i] = v[j];
       v[j] = t;
     }
   }
-#pragma unroll
-  for (int len = 2; len <= N; len <<= 1) {
-#pragma unroll
-    for (int i = 0; i < N; i += len)
-#pragma unroll
-      for (int j = 0; j < len / 2; ++j) {
-        cpx<T> w = ts[j * (N / len)];
-        if (inverse) w.im = -w.im;
-        const cpx<T> u = v[i + j];
-        const cpx<T> t = cmulc(w, v[i + j + len / 2]);
-        v[i + j] = cadd(u, t);
-        v[i + j + len / 2] = csub(u, t);
-      }
-  }
+  if constexpr (N >= 2) reg_fft_stage<T, N, TS, 2>(v, ts, inverse);
 }
 
 // tw[k] = exp(-2 pi i k / n), k < n, computed in fp64 with exact argument reduction
@@ -93,6 +111,136 @@ struct SolveSpec {
   int64_t lo_base = 0;  // global index of local lo-element 0 (the all-to-all layout of a
                         // sharded solve: this rank's slice of the axes before the last)
 };
+
+// Four-step C2C pass for N = P * N2 points (P <= N2, both powers of two), in
+// place: n = n1 + P n2, k = k2 + N2 k1.  A line is served by P threads; thread
+// n1 holds x[n1 + P n2] (n2 < N2) in registers, runs the inner N2-point FFT,
+// applies W_N^(n1 k2), and the line's P x N2 matrix is transposed through
+// shared memory so that each thread ends with N2 / P columns k2 = n1 + P c of
+// all P rows for the outer P-point FFTs: X[k2 + N2 k1].  Two register FFTs and
+// one shared-memory exchange per pass -- against four smem round trips of the
+// radix-8 tile kernel.
+//   STRIDED = false: contiguous lines (line l at l * N); a warp reads and
+//     writes 32 / P runs of P consecutive points.  P >= 8.
+//   STRIDED = true: lines at lo-stride st (element (lo, k) at lo + st (k + N h));
+//     the 256 / P lines of a CTA are consecutive lo, so a warp reads and writes
+//     32 consecutive lo of one point.  P <= 8.
+// `ss.active` (the last-axis pass of the solve): forward, divide by
+// 1 + sum_k 4 sin^2, inverse (through one more exchange), as k_fft_t.
+template <int N2>
+__host__ __device__ constexpr int fft4_smem_cpx() {
+  return N2 + 256 * (N2 + 1);  // N2-point table + exchange
+}
+
+// One four-step transform of the register line v (input layout: v[j] =
+// x[n1 + P j], n1 = this thread's row) into u (output layout: u[c][k1] =
+// X[k2 + N2 k1], k2 = n1 + P c) through the exchange buffer.
+template <typename T, int P, int N2, bool STRIDED>
+__device__ __forceinline__ int fft4_xa(int g, int n1, int k2) {
+  return STRIDED ? (n1 * N2 + k2) * (256 / P) + g : g * (P * (N2 + 1)) + n1 * (N2 + 1) + k2;
+}
+
+template <typename T, int P, int N2, bool STRIDED>
+__device__ __forceinline__ void four_step(cpx<T> (&v)[N2], cpx<T> (&u)[N2 / P][P],
+                                          const cpx<T>* tsn, const cpx<T>* __restrict__ tw,
+                                          cpx<T>* xch, int g, int p, bool inv) {
+  constexpr int N = N2 * P, CP = N2 / P;
+  reg_fft<T, N2>(v, tsn, inv);
+#pragma unroll
+  for (int k2 = 1; k2 < N2; ++k2) {  // W_N^(n1 k2)
+    cpx<T> w = tw[(p * k2) % N];
+    if (inv) w.im = -w.im;
+    v[k2] = cmulc(v[k2], w);
+  }
+#pragma unroll
+  for (int k2 = 0; k2 < N2; ++k2) xch[fft4_xa<T, P, N2, STRIDED>(g, p, k2)] = v[k2];
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < CP; ++c)
+#pragma unroll
+    for (int n1 = 0; n1 < P; ++n1) u[c][n1] = xch[fft4_xa<T, P, N2, STRIDED>(g, n1, p + P * c)];
+#pragma unroll
+  for (int c = 0; c < CP; ++c) reg_fft<T, P, N2 / P>(u[c], tsn, inv);
+}
+
+template <typename T, int P, int N2, bool STRIDED, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_fft4(cpx<T>* __restrict__ data, int64_t st,
+                                                    int64_t hi, const cpx<T>* __restrict__ tw,
+                                                    int inverse, SolveSpec ss,
+                                                    const double* __restrict__ lam) {
+  constexpr int N = N2 * P, G = 256 / P, CP = N2 / P;
+  static_assert(P <= N2, "four-step split");
+  static_assert(STRIDED ? P <= 8 : P >= 8, "layout / coalescing constraint");
+  extern __shared__ __align__(16) unsigned char fft4_smem[];
+  cpx<T>* tsn = reinterpret_cast<cpx<T>*>(fft4_smem);
+  cpx<T>* xch = tsn + N2;
+  __shared__ double den[G];
+  const int tid = threadIdx.x;
+  const int p = STRIDED ? tid / G : tid % P;
+  const int g = STRIDED ? tid % G : tid / P;
+  for (int k = tid; k < N2; k += 256) tsn[k] = tw[k * P];  // W_N2^k = W_N^(P k)
+  const int64_t nlines = STRIDED ? st * hi : hi;
+  const int64_t ntiles = (nlines + G - 1) / G;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t line = tile * G + g;
+    const bool ok = line < nlines;
+    int64_t base, es;
+    if (STRIDED) {
+      const int64_t lo = line % st, h = line / st;
+      base = lo + st * (int64_t)N * h;
+      es = st;
+    } else {
+      base = line * (int64_t)N;
+      es = 1;
+    }
+    __syncthreads();  // table ready / previous tile's exchange reads done
+    cpx<T> v[N2];
+#pragma unroll
+    for (int j = 0; j < N2; ++j)
+      v[j] = ok ? data[base + es * (p + P * j)] : cpx<T>{T(0), T(0)};
+    cpx<T> u[CP][P];
+    if (!ss.active) {
+      four_step<T, P, N2, STRIDED>(v, u, tsn, tw, xch, g, p, inverse != 0);
+    } else {
+      if (p == 0) {
+        double dsum = 1.0;
+        int64_t rem = ss.lo_base + (STRIDED ? line % st : 0);
+        for (int a = 0; a < ss.d - 1; ++a) {
+          const int64_t j = rem % ss.dims[a];
+          rem /= ss.dims[a];
+          if (ss.lam_off[a] >= 0) dsum += lam[ss.lam_off[a] + j];
+        }
+        den[g] = dsum;
+      }
+      four_step<T, P, N2, STRIDED>(v, u, tsn, tw, xch, g, p, false);
+      // X[k2 + N2 k1], k2 = p + P c: divide, then back to the input layout
+      // (natural k = n1' + P n2' at row k % P, column k / P) for the inverse
+      __syncthreads();  // exchange reads done before it is rewritten; den ready
+      const double dl = den[g];
+      const int lo_off = ss.lam_off[ss.d - 1];
+#pragma unroll
+      for (int c = 0; c < CP; ++c)
+#pragma unroll
+        for (int k1 = 0; k1 < P; ++k1) {
+          const int k = p + P * c + N2 * k1;
+          const T sc = (T)(1.0 / (dl + (lo_off >= 0 ? lam[lo_off + k] : 0.0)));
+          xch[fft4_xa<T, P, N2, STRIDED>(g, k % P, k / P)] =
+              cpx<T>{u[c][k1].re * sc, u[c][k1].im * sc};
+        }
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < N2; ++j) v[j] = xch[fft4_xa<T, P, N2, STRIDED>(g, p, j)];
+      __syncthreads();
+      four_step<T, P, N2, STRIDED>(v, u, tsn, tw, xch, g, p, true);
+    }
+    if (ok) {
+#pragma unroll
+      for (int c = 0; c < CP; ++c)
+#pragma unroll
+        for (int k1 = 0; k1 < P; ++k1) data[base + es * (p + P * c + N2 * k1)] = u[c][k1];
+    }
+  }
+}
 
 // C2C pass along a short power-of-two axis (N <= 32) with lo-stride st >= 32,
 // in place: one thread per line, the whole line in registers, every load and

@@ -3,7 +3,7 @@
 TR_SERIAL_MODES=1 python tools/sweep_profile.py [sweeps]
 With TR_SERIAL_MODES the per-mode LRTA chains run on one stream, so every
 category time is the kernel's own (uncontended) duration.  Also prints the
-iterative small-solver counters (g_dbg: ritz sweeps, face-SVT sweeps).
+launch count.
 """
 
 import ctypes
@@ -22,7 +22,6 @@ from paper_2506_09594_b200.tensors import ColMajor  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 dims = bench.WORKLOAD["dims"]
 lib = _lib.lib()
-lib.tr_debug_read.argtypes = [ctypes.POINTER(ctypes.c_int), ctypes.c_int]
 flat = bench.make_workload(torch, dims, 1234)
 cm = ColMajor(flat, dims, "torch", None)
 mask = torch.ones(flat.numel(), dtype=torch.uint8, device="cuda")
@@ -32,8 +31,6 @@ cfg = pk.SolverConfig(phi=pk.MCP(2.5), psi=pk.MCP(2.5), randomized=True, sketch=
 run = NativeSolver("gnrhtc", cm, None, mask, cfg, bench.WORKLOAD["modes"], cfg.lam_for(dims))
 for _ in range(3):
     run.step()
-dbg = (ctypes.c_int * 8)()
-lib.tr_debug_read(dbg, 1)
 torch.cuda.synchronize()
 lib.tr_profile_enable(1)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -44,11 +41,9 @@ e1.record()
 torch.cuda.synchronize()
 prof = _lib.profile_read()
 lib.tr_profile_enable(0)
-lib.tr_debug_read(dbg, 1)
 print(f"serial={os.environ.get('TR_SERIAL_MODES') is not None}  ms/sweep {e0.elapsed_time(e1) / n:.3f}")
 tot = 0.0
 for k, (ms, cnt) in sorted(prof.items(), key=lambda x: -x[1][0]):
     tot += ms / n
     print(f"  {k:18s} {ms / n * 1e3:9.1f} us/sweep  {cnt / n:6.1f} launches/sweep")
-print(f"  sum {tot:.3f} ms;  dbg per sweep: {[round(d / n, 1) for d in dbg]}")
 run.close()
