@@ -178,10 +178,36 @@ static FftTileKernel<T> fft_tile_kernel(int ln) {
 // One persistent power-of-two pass (nt = points per line, 8 <= nt <= 2048):
 // the compile-time specialised kernel when the tile holds exactly 2048
 // points, the runtime-shaped k_fft_p2 otherwise.  Grid = resident CTAs.
+// k_fft4_real for the axis-0 real passes of a 1024-point first mode (swapped
+// half-spectrum layout); false otherwise
+template <typename T, int MINB>
+static void fft4_real_launch(int mode, const void* in, void* dst, double scale, int64_t lines,
+                             int64_t tr_n1, const cpx<T>* tw, cudaStream_t st) {
+  const size_t smem = (size_t)fft4_smem_cpx<32>() * sizeof(cpx<T>);
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    cudaFuncSetAttribute(k_fft4_real<T, 16, 32, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fft4_real<T, 16, 32, MINB>, 256,
+                                                  smem);
+    per_sm = std::max(per_sm, 1);
+  }
+  const unsigned grid = (unsigned)std::min<int64_t>(cdiv(lines, 16), (int64_t)per_sm * num_sms());
+  launch("fft", k_fft4_real<T, 16, 32, MINB>, grid, 256, smem, st, in, dst, mode, scale, lines,
+         tr_n1, tw);
+}
+
 template <typename T>
 static void fft_pass_p2(int mode, const void* in, void* dst, double scale, int64_t stv, int n,
                         int64_t hi, const cpx<T>* tw, int inverse, const SolveSpec& ss,
                         const double* lam, int64_t tr_n1, cudaStream_t st) {
+  static const bool no4 = getenv("TR_NO_FFT4") != nullptr || getenv("TR_NO_FFT4_REAL") != nullptr;
+  static const int mb = getenv("TR_FFT4R_MINB") ? atoi(getenv("TR_FFT4R_MINB")) : 2;
+  if (!no4 && mode != FFT_C2C && n == 1024 && tr_n1 > 0 && stv == 1 && !ss.active) {
+    if (mb == 2) fft4_real_launch<T, 2>(mode, in, dst, scale, hi, tr_n1, tw, st);
+    else fft4_real_launch<T, 1>(mode, in, dst, scale, hi, tr_n1, tw, st);
+    return;
+  }
   const int nt = mode == FFT_C2C ? n : n / 2;
   int ln = 0;
   while ((1 << ln) < nt) ++ln;

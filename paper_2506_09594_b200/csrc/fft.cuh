@@ -36,6 +36,8 @@ __device__ __forceinline__ cpx<T> cmulc(cpx<T> a, cpx<T> b) {
 template <typename T>
 __device__ __forceinline__ cpx<T> cconjt(cpx<T> a) { return {a.re, -a.im}; }
 
+enum FftMode { FFT_C2C = 0, FFT_R2C = 1, FFT_C2R = 2 };
+
 __host__ __device__ constexpr int bitrev_c(int i, int bits) {
   return bits == 0 ? 0 : (((i & 1) << (bits - 1)) | bitrev_c(i >> 1, bits - 1));
 }
@@ -140,15 +142,17 @@ __device__ __forceinline__ int fft4_xa(int g, int n1, int k2) {
   return STRIDED ? (n1 * N2 + k2) * (256 / P) + g : g * (P * (N2 + 1)) + n1 * (N2 + 1) + k2;
 }
 
-template <typename T, int P, int N2, bool STRIDED>
-__device__ __forceinline__ void four_step(cpx<T> (&v)[N2], cpx<T> (&u)[N2 / P][P],
-                                          const cpx<T>* tsn, const cpx<T>* __restrict__ tw,
-                                          cpx<T>* xch, int g, int p, bool inv) {
+// (twiddles W_N^m read as tw[TWS m]: the n0-point table of a real pass serves
+// its N = n0 / 2-point complex transform with TWS = 2)
+template <typename T, int P, int N2, bool STRIDED, int TWS>
+__device__ __forceinline__ void four_step_tw(cpx<T> (&v)[N2], cpx<T> (&u)[N2 / P][P],
+                                             const cpx<T>* tsn, const cpx<T>* __restrict__ tw,
+                                             cpx<T>* xch, int g, int p, bool inv) {
   constexpr int N = N2 * P, CP = N2 / P;
   reg_fft<T, N2>(v, tsn, inv);
 #pragma unroll
   for (int k2 = 1; k2 < N2; ++k2) {  // W_N^(n1 k2)
-    cpx<T> w = tw[(p * k2) % N];
+    cpx<T> w = tw[TWS * ((p * k2) % N)];
     if (inv) w.im = -w.im;
     v[k2] = cmulc(v[k2], w);
   }
@@ -161,6 +165,13 @@ __device__ __forceinline__ void four_step(cpx<T> (&v)[N2], cpx<T> (&u)[N2 / P][P
     for (int n1 = 0; n1 < P; ++n1) u[c][n1] = xch[fft4_xa<T, P, N2, STRIDED>(g, n1, p + P * c)];
 #pragma unroll
   for (int c = 0; c < CP; ++c) reg_fft<T, P, N2 / P>(u[c], tsn, inv);
+}
+
+template <typename T, int P, int N2, bool STRIDED>
+__device__ __forceinline__ void four_step(cpx<T> (&v)[N2], cpx<T> (&u)[N2 / P][P],
+                                          const cpx<T>* tsn, const cpx<T>* __restrict__ tw,
+                                          cpx<T>* xch, int g, int p, bool inv) {
+  four_step_tw<T, P, N2, STRIDED, 1>(v, u, tsn, tw, xch, g, p, inv);
 }
 
 template <typename T, int P, int N2, bool STRIDED, int MINB>
@@ -238,6 +249,124 @@ __global__ void __launch_bounds__(256, MINB) k_fft4(cpx<T>* __restrict__ data, i
       for (int c = 0; c < CP; ++c)
 #pragma unroll
         for (int k1 = 0; k1 < P; ++k1) data[base + es * (p + P * c + N2 * k1)] = u[c][k1];
+    }
+  }
+}
+
+// Axis-0 real passes of the solve with the four-step core: a real line of
+// n0 = 2N points is the complex line z[j] = x[2j] + i x[2j+1] of N = P N2
+// points.
+//   R2C: Z = FFT_N(z), then X[k] = E + w^k O, X[N-k] = conj(E - w^k O) with
+//        E = (Z[k] + conj Z[N-k]) / 2, O = -i (Z[k] - conj Z[N-k]) / 2, w the
+//        n0-point root; the N + 1 bins go to the half spectrum in the swapped
+//        layout: bin k of line (i1, rest) at i1 + tr_n1 (k + (N+1) rest).
+//   C2R: the inverse (Z[k] = E + i O from the bin pairs, inverse FFT_N, the
+//        real line scaled by out_scale).
+// G = 256 / P lines per CTA (consecutive i1), so every bin of the half
+// spectrum is read / written as G consecutive complex values.
+template <typename T, int P, int N2, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_fft4_real(const void* in, void* out, int mode,
+                                                         double out_scale, int64_t lines,
+                                                         int64_t tr_n1,
+                                                         const cpx<T>* __restrict__ tw) {
+  // natural-order staging stride NB = N + 1 = 1 mod 16 complex: the G lines of
+  // one bin fall in distinct banks
+  constexpr int N = P * N2, G = 256 / P, CP = N2 / P, NB = N + 1, LS = NB;
+  static_assert(G * LS <= 256 * (N2 + 1), "staging fits the exchange buffer");
+  extern __shared__ __align__(16) unsigned char fft4_smem[];
+  cpx<T>* tsn = reinterpret_cast<cpx<T>*>(fft4_smem);
+  cpx<T>* xch = tsn + N2;
+  const int tid = threadIdx.x;
+  const int p = tid % P, g = tid / P;
+  for (int k = tid; k < N2; k += 256) tsn[k] = tw[2 * k * P];  // W_N2 = W_n0^(2 P)
+  // the N-point table of the inner four-step: W_N^m = W_n0^(2 m)
+  const int64_t ntiles = (lines + G - 1) / G;
+  const T osc = (T)out_scale;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t line0 = tile * G;
+    __syncthreads();
+    cpx<T> v[N2];
+    cpx<T> u[CP][P];
+    if (mode == FFT_R2C) {
+      const int64_t line = line0 + g;
+      const bool ok = line < lines;
+      const cpx<T>* zl = reinterpret_cast<const cpx<T>*>(in) + line * (int64_t)N;
+#pragma unroll
+      for (int j = 0; j < N2; ++j) v[j] = ok ? zl[p + P * j] : cpx<T>{T(0), T(0)};
+      four_step_tw<T, P, N2, false, 2>(v, u, tsn, tw, xch, g, p, false);
+      __syncthreads();
+#pragma unroll
+      for (int c = 0; c < CP; ++c)
+#pragma unroll
+        for (int k1 = 0; k1 < P; ++k1) xch[g * LS + p + P * c + N2 * k1] = u[c][k1];
+      __syncthreads();
+      // bins k = 0 .. N (pairs k, N - k): thread -> (line t % G, bin t / G + step j)
+      cpx<T>* Xo = reinterpret_cast<cpx<T>*>(out);
+      const int gl = tid % G;
+      const int64_t ln = line0 + gl;
+      if (ln < lines) {
+        const int64_t lb = (ln % tr_n1) + tr_n1 * (int64_t)NB * (ln / tr_n1);
+        for (int k = tid / G; k <= N / 2; k += P) {
+          const cpx<T> a = xch[gl * LS + k];
+          const cpx<T> bb = cconjt(xch[gl * LS + ((N - k) & (N - 1))]);
+          const cpx<T> E = {(a.re + bb.re) * T(0.5), (a.im + bb.im) * T(0.5)};
+          const cpx<T> D = {(a.re - bb.re) * T(0.5), (a.im - bb.im) * T(0.5)};
+          const cpx<T> O = {D.im, -D.re};
+          const cpx<T> WO = cmulc(tw[k], O);
+          Xo[lb + tr_n1 * k] = cadd(E, WO);
+          if (k < N / 2 || k == 0) Xo[lb + tr_n1 * (N - k)] = {E.re - WO.re, WO.im - E.im};
+        }
+      }
+    } else {
+      // C2R: stage the N + 1 bins of the G lines, pair them into Z in place
+      const cpx<T>* Xi = reinterpret_cast<const cpx<T>*>(in);
+      const int gl = tid % G;
+      const int64_t ln = line0 + gl;
+      if (ln < lines) {
+        const int64_t lb = (ln % tr_n1) + tr_n1 * (int64_t)NB * (ln / tr_n1);
+        constexpr int IT = (NB + P - 1) / P;
+        cpx<T> st[IT];  // all loads in flight before the shared-memory stores
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+          const int k = tid / G + P * it;
+          if (k < NB) st[it] = Xi[lb + tr_n1 * k];
+        }
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+          const int k = tid / G + P * it;
+          if (k < NB) xch[gl * LS + k] = st[it];
+        }
+      }
+      __syncthreads();
+      if (ln < lines)
+        for (int k = tid / G; k <= N / 2; k += P) {
+          // Z[k] = E + i O, Z[N-k] = conj(E - i O) with E = (X[k] + conj X[N-k]) / 2,
+          // O = conj(w^k) (X[k] - conj X[N-k]) / 2
+          const cpx<T> a = xch[gl * LS + k];
+          const cpx<T> bb = cconjt(xch[gl * LS + N - k]);
+          const cpx<T> E = {(a.re + bb.re) * T(0.5), (a.im + bb.im) * T(0.5)};
+          const cpx<T> D = {(a.re - bb.re) * T(0.5), (a.im - bb.im) * T(0.5)};
+          const cpx<T> O = cmulc(D, cconjt(tw[k]));
+          const cpx<T> z1 = {E.re - O.im, E.im + O.re};
+          const cpx<T> z2 = {E.re + O.im, O.re - E.im};
+          xch[gl * LS + k] = z1;
+          if (k > 0 && k < N / 2) xch[gl * LS + N - k] = z2;
+          if (k == N / 2) xch[gl * LS + k] = z1;
+        }
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < N2; ++j) v[j] = xch[g * LS + p + P * j];
+      __syncthreads();
+      four_step_tw<T, P, N2, false, 2>(v, u, tsn, tw, xch, g, p, true);
+      const int64_t line = line0 + g;
+      if (line < lines) {
+        cpx<T>* zo = reinterpret_cast<cpx<T>*>(out) + line * (int64_t)N;
+#pragma unroll
+        for (int c = 0; c < CP; ++c)
+#pragma unroll
+          for (int k1 = 0; k1 < P; ++k1)
+            zo[p + P * c + N2 * k1] = cpx<T>{u[c][k1].re * osc, u[c][k1].im * osc};
+      }
     }
   }
 }
@@ -487,7 +616,6 @@ __device__ __forceinline__ void lines_fft(cpx<T>* buf, cpx<T>* tmp, int L, int n
 }
 
 // Pass modes
-enum FftMode { FFT_C2C = 0, FFT_R2C = 1, FFT_C2R = 2 };
 
 
 // One pass along an axis.
