@@ -15,6 +15,7 @@
 #include "panel_mma.cuh"
 #include "orth_cluster.cuh"
 #include "proj_tc.cuh"
+#include "expand_tc.cuh"
 #include "prof.cuh"
 
 namespace tr {
@@ -115,6 +116,7 @@ struct Bufs {
   int64_t* rpi;
   double *tq_tau, *tq_R, *tq_C;
   float *zhi, *zlo;
+  float *c1h, *c1l, *f0h, *f0l;  // tcgen05 expand operands (K-major, K = 32, tf32 hi / lo)
   int64_t max_parts, max_mparts;
 };
 
@@ -182,6 +184,11 @@ static void carve(Carve& cv, const Shape& sh, Bufs<T>& b) {
   b.tq_C = cv.take<double>(tq_rows * smax);
   b.zhi = cv.take<float>(mmax * 32);
   b.zlo = cv.take<float>(mmax * 32);
+  const bool tc_expand = sizeof(T) == 4 && sh.r0 <= 32;
+  b.c1h = cv.take<float>(tc_expand ? sh.n2 * sh.nf * 32 : 1);
+  b.c1l = cv.take<float>(tc_expand ? sh.n2 * sh.nf * 32 : 1);
+  b.f0h = cv.take<float>(tc_expand ? sh.n1 * 32 : 1);
+  b.f0l = cv.take<float>(tc_expand ? sh.n1 * 32 : 1);
 }
 
 template <typename T, int B>
@@ -644,8 +651,42 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
   return 0;
 }
 
+// out = F0 C1 on the tensor cores (expand_tc.cuh) when the shapes suit it
+static bool expand_tc(const Shape& sh, Bufs<float>& bf, float* out, cudaStream_t st) {
+  static const bool off = getenv("TR_NO_EXPAND_TC") != nullptr;
+  const int64_t N = sh.n2 * sh.nf;
+  if (off || sh.r0 > 32 || sh.n1 % 128 != 0 || N >= (1ll << 31) || sh.n1 >= (1ll << 31))
+    return false;
+  CUtensorMap ah, al, bh, bl;
+  if (!tmap_f32(&ah, bf.f0h, 32, sh.n1, 128) || !tmap_f32(&al, bf.f0l, 32, sh.n1, 128) ||
+      !tmap_f32(&bh, bf.c1h, 32, N, 128) || !tmap_f32(&bl, bf.c1l, 32, N, 128))
+    return false;
+  launch("expand_mode1", k_expand_mode1_split, (unsigned)(cdiv(sh.n2, 128) * sh.nf), 128, 0, st,
+         (const double*)(bf.core + sh.r0 * sh.r1 * sh.f0), (int)sh.r0, (int)sh.r1, sh.nf,
+         (const double*)bf.F1, sh.n2, bf.c1h, bf.c1l);
+  launch("expand_split", k_split_rows, (unsigned)cdiv(sh.n1 * 32, 256), 256, 0, st,
+         (const double*)bf.F0, sh.n1, (int)sh.r0, bf.f0h, bf.f0l);
+  const int64_t nrb = sh.n1 / 128;
+  const int64_t per = std::max<int64_t>(1, std::min<int64_t>(stream_sms() / nrb, cdiv(N, 128)));
+  const size_t smem = (size_t)kEtSmemBytes + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_expand_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  launch("gemm_expand", k_expand_tc, (unsigned)(per * nrb), kEtThreads, smem, st, ah, al, bh, bl,
+         sh.n1, N, out);
+  return true;
+}
+
+static bool expand_tc(const Shape&, Bufs<double>&, double*, cudaStream_t) { return false; }
+
 template <typename T>
 static int expand(const Shape& sh, Bufs<T>& bf, T* out, cudaStream_t st) {
+  if (expand_tc(sh, bf, out, st)) {
+    TR_LAUNCH_CHECK();
+    return 0;
+  }
   const int64_t N = sh.n2 * sh.nf;
   launch("expand_mode1", k_expand_mode1<T>, (unsigned)(cdiv(sh.n2, 128) * sh.nf), 128, 0, st,
          (const double*)(bf.core + sh.r0 * sh.r1 * sh.f0), (int)sh.r0, (int)sh.r1, sh.nf, bf.F1,

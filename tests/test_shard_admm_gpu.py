@@ -53,13 +53,18 @@ def test_world1_sharded_matches_unsharded(cuda_lib, dims):
     mobs, mask = _problem(dims)
     cfg = _cfg(pk, 5)
     l0, e0, r0 = pk.gnrhtc(mobs, mask, cfg)
-    if not dist.is_initialized():
+    own = not dist.is_initialized()
+    if own:
         with socket.socket() as s:
             s.bind(("127.0.0.1", 0))
             port = s.getsockname()[1]
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0,
                                 world_size=1)
-    l1, e1, r1 = pk.gnrhtc_sharded(mobs, mask, cfg, dims[-1], 0)
+    try:
+        l1, e1, r1 = pk.gnrhtc_sharded(mobs, mask, cfg, dims[-1], 0)
+    finally:
+        if own:
+            dist.destroy_process_group()
     assert _rel(l1, l0) <= 1e-12 and _rel(e1, e0) <= 1e-12
     np.testing.assert_allclose(np.array(r1.residual_history), np.array(r0.residual_history),
                                rtol=1e-10, atol=1e-14)
