@@ -523,7 +523,7 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-BLBP_EPS, BLBP_BLOCK = 0.35, 8
+BLBP_EPS, BLBP_BLOCK = 0.45, 8
 
 
 def fp64_leg(torch, pk, NativeSolver, ColMajor, lib, flat, dims, mask_dev, steps):

@@ -995,6 +995,10 @@ static int admm_create(const AdmmConfig& cfg, int order, const int64_t* dims, co
   }
   const int64_t N = g.N;
   const int nm = cfg.nmodes;
+  {
+    static const bool mem_order = getenv("TR_WALK_MEMORY_ORDER") != nullptr;
+    if (!mem_order && order >= 3) g.walk_last = dims[order - 1];
+  }
   if (s->sharded) {
     g.halo = order - 1;
     s->face = N / s->nl;

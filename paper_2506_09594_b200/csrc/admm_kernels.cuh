@@ -28,6 +28,12 @@ struct Geom {
   // neighbouring ranks, so the circular neighbour of a boundary face is the
   // ghost (no local wrap).  -1: every axis is whole and periodic.
   int halo = -1;
+  // line-walk order of the resident line kernels (for_each_chunk): with
+  // walk_last > 1 the last axis is visited fastest, so a line's neighbours
+  // along the last axis -- whole faces (MBs) apart in memory -- are the
+  // previous / next line of the walk and still in L2, while the ones along
+  // the inner axes stay within a few MB of the walk.  0: memory order.
+  int64_t walk_last = 0;
 };
 
 // offsets of the previous / next element along axis a (a >= 1) for a line
@@ -146,7 +152,9 @@ __device__ __forceinline__ void for_each_chunk(const Geom& g, F&& f) {
   const int cpl = (int)(n0 / V);
   LineCo lc;
   if (cpl >= (int)blockDim.x) {
-    for (int64_t line = blockIdx.x; line < lines; line += gridDim.x) {
+    const int64_t wl = g.walk_last, per = wl > 1 ? lines / wl : lines;
+    for (int64_t v = blockIdx.x; v < lines; v += gridDim.x) {
+      const int64_t line = wl > 1 ? (v % wl) * per + v / wl : v;
       lc.line = line;
       for (int a = 1; a < g.d; ++a) lc.co[a] = (int)line_coord(g, line, a);
       for (int c = threadIdx.x; c < cpl; c += blockDim.x) f(lc, (int64_t)c * V);

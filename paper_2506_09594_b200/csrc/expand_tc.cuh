@@ -52,12 +52,15 @@ __device__ __forceinline__ void tmem_ld64(uint32_t taddr, float (&v)[64]) {
   for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-constexpr int kEtStages = 5;
+constexpr int kEtStages = 5;        // C1 ring depth (direct-store epilogue)
+constexpr int kEtStagesTs = 3;      // C1 ring depth next to the TMA-store staging
 constexpr int kEtEpiWarps = 16;  // 4 per TMEM lane quarter, 128 / 4 columns each
 constexpr int kEtThreads = 64 + 32 * kEtEpiWarps;  // producer, MMA, epilogue warps
 constexpr int kEtABytes = 128 * 128;          // 128 rows x 32 fp32
 constexpr int kEtStageBytes = 2 * 128 * 128;  // C1_hi + C1_lo tile
 constexpr int kEtSmemBytes = 2 * kEtABytes + kEtStages * kEtStageBytes;
+// TMA-store variant: 3 ring stages + one 32 x 32 fp32 staging box per epilogue warp
+constexpr int kEtSmemBytesTs = 2 * kEtABytes + kEtStagesTs * kEtStageBytes + kEtEpiWarps * 4096;
 
 // rows (K-major, 32-float rows): hi[r * 32 + k] = tf32(x), lo = x - hi, for the
 // n x K fp64 column-major factor F (zero for k >= K)
@@ -112,17 +115,37 @@ __global__ void __launch_bounds__(128) k_expand_mode1_split(const double* __rest
   }
 }
 
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+          (uint64_t)map),
+      "r"(c0), "r"(c1), "r"(src)
+      : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+__device__ __forceinline__ void tma_store_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+// TS: the epilogue stages each warp's 32 x 32 block in shared memory and
+// writes it with a TMA tensor store (mapOut: out, n1 x N, box 32 x 32);
+// otherwise direct coalesced st.global.
+template <bool TS>
 __global__ void __launch_bounds__(kEtThreads, 1)
     k_expand_tc(const __grid_constant__ CUtensorMap mapAh, const __grid_constant__ CUtensorMap mapAl,
                 const __grid_constant__ CUtensorMap mapBh, const __grid_constant__ CUtensorMap mapBl,
-                int64_t n1, int64_t N, float* __restrict__ out) {
+                const __grid_constant__ CUtensorMap mapOut, int64_t n1, int64_t N,
+                float* __restrict__ out) {
+  constexpr int NST = TS ? kEtStagesTs : kEtStages;
   extern __shared__ __align__(1024) unsigned char et_raw[];
-  __shared__ __align__(8) uint64_t full[kEtStages], empty[kEtStages], abar;
+  __shared__ __align__(8) uint64_t full[NST], empty[NST], abar;
   __shared__ __align__(8) uint64_t tfull[2], tempty[2];
   __shared__ uint32_t tmem_base_s;
   unsigned char* smem = (unsigned char*)(((uintptr_t)et_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = smem_u32(smem);
   const uint32_t sAh = sbase, sAl = sbase + kEtABytes, sB = sbase + 2 * kEtABytes;
+  (void)out;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nrb = (int)(n1 / 128);
   const int rb = (int)(blockIdx.x % nrb);
@@ -137,7 +160,7 @@ __global__ void __launch_bounds__(kEtThreads, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kEtStages; ++i) {
+    for (int i = 0; i < NST; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
@@ -159,8 +182,8 @@ __global__ void __launch_bounds__(kEtThreads, 1)
       tma_load_2d(sAh, &mapAh, 0, rb * 128, &abar);
       tma_load_2d(sAl, &mapAl, 0, rb * 128, &abar);
       for (int64_t t = 0; t < my_tiles; ++t) {
-        const int st = (int)(t % kEtStages);
-        const uint32_t ph = (uint32_t)((t / kEtStages) & 1);
+        const int st = (int)(t % NST);
+        const uint32_t ph = (uint32_t)((t / NST) & 1);
         mbar_wait(&empty[st], ph ^ 1);
         const int col = (int)((c0 + t * cstride) * 128);
         const uint32_t sb = sB + (uint32_t)(st * kEtStageBytes);
@@ -177,9 +200,9 @@ __global__ void __launch_bounds__(kEtThreads, 1)
       const uint64_t dAh = umma_desc_sw128(sAh), dAl = umma_desc_sw128(sAl);
       for (int64_t t = 0; t < my_tiles; ++t) {
         const int acc = (int)(t & 1);
-        const int st = (int)(t % kEtStages);
+        const int st = (int)(t % NST);
         mbar_wait(&tempty[acc], (uint32_t)(((t >> 1) & 1) ^ 1));
-        mbar_wait(&full[st], (uint32_t)((t / kEtStages) & 1));
+        mbar_wait(&full[st], (uint32_t)((t / NST) & 1));
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(acc * 128);
         const uint64_t dBh = umma_desc_sw128(sB + (uint32_t)(st * kEtStageBytes));
@@ -209,13 +232,26 @@ __global__ void __launch_bounds__(kEtThreads, 1)
       tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * 128 + CW * part), a);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);  // the accumulator is in registers: free it early
-      if (row < n1) {
+      if (TS) {
+        // this warp's box: rows 32 q .. of the row block, columns col0 .. col0 + 31
+        float* box = reinterpret_cast<float*>(smem + 2 * kEtABytes + NST * kEtStageBytes) +
+                     (warp - 2) * 1024;
+        if (lane == 0) tma_store_wait_read();  // the previous tile's store has read the box
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < CW; ++j) box[j * 32 + lane] = a[j];
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0)
+          tma_store_2d(&mapOut, smem_u32(box), (int)(rb * 128 + 32 * q), (int)col0);
+      } else if (row < n1) {
         float* o = out + row + n1 * col0;
 #pragma unroll
         for (int j = 0; j < CW; ++j)
           if (col0 + j < N) o[n1 * j] = a[j];
       }
     }
+    if (TS && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();

@@ -167,6 +167,35 @@ __device__ __forceinline__ void four_step_tw(cpx<T> (&v)[N2], cpx<T> (&u)[N2 / P
   for (int c = 0; c < CP; ++c) reg_fft<T, P, N2 / P>(u[c], tsn, inv);
 }
 
+// The inverse of four_step straight from its output layout (u[c][k1] =
+// X[k2 + N2 k1], k2 = n1 + P c) back to the input layout (v[j] = x[n1 + P j]):
+// x[n1 + P n2] = sum_k2 W_N2^(-n2 k2) W_N^(-n1 k2) sum_k1 X[k2 + N2 k1] W_P^(-n1 k1)
+// -- outer P-point FFTs in registers, twiddle, ONE exchange, inner N2-point FFT.
+template <typename T, int P, int N2, bool STRIDED>
+__device__ __forceinline__ void four_step_inv_out(cpx<T> (&u)[N2 / P][P], cpx<T> (&v)[N2],
+                                                  const cpx<T>* tsn, const cpx<T>* __restrict__ tw,
+                                                  cpx<T>* xch, int g, int p) {
+  constexpr int N = N2 * P, CP = N2 / P;
+#pragma unroll
+  for (int c = 0; c < CP; ++c) {
+    reg_fft<T, P, N2 / P>(u[c], tsn, true);  // u[c][n1] = sum_k1 X[k2 + N2 k1] W_P^(-n1 k1)
+#pragma unroll
+    for (int n1 = 1; n1 < P; ++n1) {
+      cpx<T> w = tw[(n1 * (p + P * c)) % N];
+      w.im = -w.im;
+      u[c][n1] = cmulc(u[c][n1], w);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < CP; ++c)
+#pragma unroll
+    for (int n1 = 0; n1 < P; ++n1) xch[fft4_xa<T, P, N2, STRIDED>(g, n1, p + P * c)] = u[c][n1];
+  __syncthreads();
+#pragma unroll
+  for (int k2 = 0; k2 < N2; ++k2) v[k2] = xch[fft4_xa<T, P, N2, STRIDED>(g, p, k2)];
+  reg_fft<T, N2>(v, tsn, true);
+}
+
 template <typename T, int P, int N2, bool STRIDED>
 __device__ __forceinline__ void four_step(cpx<T> (&v)[N2], cpx<T> (&u)[N2 / P][P],
                                           const cpx<T>* tsn, const cpx<T>* __restrict__ tw,
@@ -224,8 +253,7 @@ __global__ void __launch_bounds__(256, MINB) k_fft4(cpx<T>* __restrict__ data, i
         den[g] = dsum;
       }
       four_step<T, P, N2, STRIDED>(v, u, tsn, tw, xch, g, p, false);
-      // X[k2 + N2 k1], k2 = p + P c: divide, then back to the input layout
-      // (natural k = n1' + P n2' at row k % P, column k / P) for the inverse
+      // X[k2 + N2 k1], k2 = p + P c: divide, then the inverse from this layout
       __syncthreads();  // exchange reads done before it is rewritten; den ready
       const double dl = den[g];
       const int lo_off = ss.lam_off[ss.d - 1];
@@ -235,14 +263,14 @@ __global__ void __launch_bounds__(256, MINB) k_fft4(cpx<T>* __restrict__ data, i
         for (int k1 = 0; k1 < P; ++k1) {
           const int k = p + P * c + N2 * k1;
           const T sc = (T)(1.0 / (dl + (lo_off >= 0 ? lam[lo_off + k] : 0.0)));
-          xch[fft4_xa<T, P, N2, STRIDED>(g, k % P, k / P)] =
-              cpx<T>{u[c][k1].re * sc, u[c][k1].im * sc};
+          u[c][k1] = cpx<T>{u[c][k1].re * sc, u[c][k1].im * sc};
         }
-      __syncthreads();
+      four_step_inv_out<T, P, N2, STRIDED>(u, v, tsn, tw, xch, g, p);
+      if (ok) {
 #pragma unroll
-      for (int j = 0; j < N2; ++j) v[j] = xch[fft4_xa<T, P, N2, STRIDED>(g, p, j)];
-      __syncthreads();
-      four_step<T, P, N2, STRIDED>(v, u, tsn, tw, xch, g, p, true);
+        for (int j = 0; j < N2; ++j) data[base + es * (p + P * j)] = v[j];
+      }
+      continue;
     }
     if (ok) {
 #pragma unroll

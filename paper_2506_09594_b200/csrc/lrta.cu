@@ -651,15 +651,31 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
   return 0;
 }
 
+// fp32 column-major rows x cols matrix, plain (unswizzled) boxes of box_rows x box_cols
+static bool tmap_f32_plain(CUtensorMap* map, const float* base, int64_t rows, int64_t cols,
+                           int box_rows, int box_cols) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)cols};
+  const cuuint64_t strides[1] = {(cuuint64_t)rows * sizeof(float)};
+  const cuuint32_t box[2] = {(cuuint32_t)box_rows, (cuuint32_t)box_cols};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // out = F0 C1 on the tensor cores (expand_tc.cuh) when the shapes suit it
 static bool expand_tc(const Shape& sh, Bufs<float>& bf, float* out, cudaStream_t st) {
   static const bool off = getenv("TR_NO_EXPAND_TC") != nullptr;
+  static const bool direct = getenv("TR_EXPAND_DIRECT_STORE") != nullptr;
   const int64_t N = sh.n2 * sh.nf;
   if (off || sh.r0 > 32 || sh.n1 % 128 != 0 || N >= (1ll << 31) || sh.n1 >= (1ll << 31))
     return false;
-  CUtensorMap ah, al, bh, bl;
+  CUtensorMap ah, al, bh, bl, mo;
   if (!tmap_f32(&ah, bf.f0h, 32, sh.n1, 128) || !tmap_f32(&al, bf.f0l, 32, sh.n1, 128) ||
-      !tmap_f32(&bh, bf.c1h, 32, N, 128) || !tmap_f32(&bl, bf.c1l, 32, N, 128))
+      !tmap_f32(&bh, bf.c1h, 32, N, 128) || !tmap_f32(&bl, bf.c1l, 32, N, 128) ||
+      !tmap_f32_plain(&mo, out, sh.n1, N, 32, 32))
     return false;
   launch("expand_mode1", k_expand_mode1_split, (unsigned)(cdiv(sh.n2, 128) * sh.nf), 128, 0, st,
          (const double*)(bf.core + sh.r0 * sh.r1 * sh.f0), (int)sh.r0, (int)sh.r1, sh.nf,
@@ -668,14 +684,21 @@ static bool expand_tc(const Shape& sh, Bufs<float>& bf, float* out, cudaStream_t
          (const double*)bf.F0, sh.n1, (int)sh.r0, bf.f0h, bf.f0l);
   const int64_t nrb = sh.n1 / 128;
   const int64_t per = std::max<int64_t>(1, std::min<int64_t>(stream_sms() / nrb, cdiv(N, 128)));
-  const size_t smem = (size_t)kEtSmemBytes + 1024;
+  const size_t smem = (size_t)(direct ? kEtSmemBytes : kEtSmemBytesTs) + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_expand_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_expand_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kEtSmemBytes + 1024);
+    cudaFuncSetAttribute(k_expand_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kEtSmemBytesTs + 1024);
     attr = true;
   }
-  launch("gemm_expand", k_expand_tc, (unsigned)(per * nrb), kEtThreads, smem, st, ah, al, bh, bl,
-         sh.n1, N, out);
+  if (direct)
+    launch("gemm_expand", k_expand_tc<false>, (unsigned)(per * nrb), kEtThreads, smem, st, ah, al,
+           bh, bl, mo, sh.n1, N, out);
+  else
+    launch("gemm_expand", k_expand_tc<true>, (unsigned)(per * nrb), kEtThreads, smem, st, ah, al,
+           bh, bl, mo, sh.n1, N, out);
   return true;
 }
 

@@ -415,6 +415,14 @@ def ad_rsthosvd_blbp(x, eps: float, block: int = 10, defl_tol: float = None, ord
     cfg = SketchConfig(mode="fixed-accuracy", order=order, eps=eps, block=block,
                        defl_tol=defl_tol, seed=seed)
     cfg.validate(dims)
+    if defl_tol is not None:
+        # sketch.py:384-388 (checked against ||x||_F, which bounds every mode's core)
+        import warnings
+
+        nrm = float(cm.flat.double().norm())
+        if nrm > 0 and defl_tol >= nrm:
+            warnings.warn(f"deflation tolerance {defl_tol:.3e} >= unfolding norm {nrm:.3e} "
+                          f"on mode {order[0]}", stacklevel=2)
     run = TuckerRun(cm, cfg, order)
     try:
         return run.tucker_factors(cm.kind == "numpy"), run.diag

@@ -16,7 +16,8 @@ CAT = [  # (kernel-name regex, category); first match wins
     (r"k_panel_mma<\d+, 1>|k_panel<.*, 1>", "panel_gram"),
     (r"k_panel_mma<\d+, 0>|k_panel<.*, 0>", "panel_sketch"),
     (r"k_proj_ws", "proj_tc"),
-    (r"k_gemm_expand", "gemm_expand"),
+    (r"k_gemm_expand|k_expand_tc", "gemm_expand"),
+    (r"k_expand_mode1", "expand_mode1"),
     (r"k_fft", "fft"),
     (r"k_sweep_tail", "sweep_tail"),
     (r"k_lrta_input", "lrta_input"),
@@ -40,7 +41,8 @@ for r in rows[2:]:
     e = {"id": int(d["ID"]), "kernel": name}
     U = dict(zip(hdr, units))
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3,
-             "usecond": 1.0, "msecond": 1e3}
+             "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3, "B": 1.0,
+             "KB": 1e3, "MB": 1e6, "GB": 1e9}
     for m in M:
         v = d.get(m, "")
         try:
@@ -63,6 +65,12 @@ for e in kern:
         c["launches"] += 1
         c["us"] += e["duration_us"] or 0
 json.dump(dict(cat), open(prefix + "_categories.json", "w"), indent=1)
+# per-step traffic by category (bench.py roofline "traffic": newest profiles/r*/traffic.json)
+json.dump({"how": "ncu --set full of one uncontended ADMM sweep (TR_SERIAL_MODES=1 "
+                  "tools/sweep_profile.py); DRAM read + write bytes summed per category",
+           "categories": {k: {"bytes_per_step": v["bytes"], "launches": v["launches"],
+                              "us_serialised": v["us"]} for k, v in cat.items()}},
+          open(prefix + "_traffic.json", "w"), indent=1)
 for k, v in sorted(cat.items(), key=lambda x: -x[1]["us"]):
     print(f"{k:14s} launches {v['launches']:3d}  {v['us']:9.1f} us  {v['bytes'] / 1e9:7.3f} GB  "
           f"{v['bytes'] / (v['us'] * 1e-6) / 1e9 if v['us'] else 0:7.1f} GB/s")
