@@ -780,6 +780,162 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+CONFIGS = {
+    2: {"workload": "completion-512x512x16x32-f32", "dims": (512, 512, 16, 32),
+        "tubal_rank": 15, "noise": 0.01, "observed": 0.10, "ranks": (25, 25), "blocks": (9, 9),
+        "krylov": (2, 2), "solver": "gnhtc",
+        "note": "BASELINE configs[2]: order-4 completion, transform along modes 3 and 4, q = 2, "
+                "p = 10 (target rank 15 + 10)"},
+    3: {"workload": "onebit-2048x2048x64-f32", "dims": (2048, 2048, 64), "tubal_rank": 10,
+        "observed": 0.50, "ranks": (15, 15), "blocks": (5, 5), "krylov": (2, 2),
+        "solver": "gnobhtc", "theta": 1.5, "sigma": 0.1,
+        "note": "BASELINE configs[3]: one-bit recovery, 50% sampled, q = 2, p = 5 (target rank "
+                "10 + 5); dithered signs (theta 1.5, Gaussian noise 0.1) as in tenrec.onebit"},
+}
+
+
+def make_tproduct(torch, dims, r, seed):
+    """Gaussian factors n1 x r x trailing and r x n2 x trailing, t-product along
+    every trailing mode (FFT over the trailing axes), unit RMS; column-major flat."""
+    n1, n2 = dims[0], dims[1]
+    tr = tuple(dims[2:])
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    a = torch.randn(tr[::-1] + (r, n1), generator=g, device="cuda")  # (..., k, i)
+    b = torch.randn(tr[::-1] + (n2, r), generator=g, device="cuda")  # (..., j, k)
+    ax = tuple(range(len(tr)))
+    fa, fb = torch.fft.fftn(a, dim=ax), torch.fft.fftn(b, dim=ax)
+    x = torch.fft.ifftn(torch.matmul(fb, fa), dim=ax).real  # (..., j, i): column-major
+    x = x / x.pow(2).mean().sqrt()
+    return x.reshape(-1).contiguous(), g
+
+
+def run_config(args):
+    """One ADMM sweep of BASELINE configs[2] or configs[3] (N = 1; same line
+    contract as the default step; e2e through gnhtc / gnobhtc with host arrays)."""
+    import numpy as np
+    import torch
+
+    import paper_2506_09594_b200 as pk
+    from paper_2506_09594_b200 import _lib
+    from paper_2506_09594_b200.solvers import NativeSolver
+    from paper_2506_09594_b200.tensors import ColMajor
+
+    C = CONFIGS[args.config]
+    torch.cuda.set_device(_env_int("LOCAL_RANK", 0))
+    lib = _lib.lib()
+    dims = C["dims"]
+    N = math.prod(dims)
+    modes = tuple(range(len(dims)))
+    x, g = make_tproduct(torch, dims, C["tubal_rank"], 4242)
+    sk = pk.SketchConfig(mode="fixed-rank", order=(0, 1), ranks=C["ranks"], blocks=C["blocks"],
+                         krylov=C["krylov"], seed=7)
+    if C["solver"] == "gnhtc":
+        x = x + C["noise"] * torch.randn(N, generator=g, device="cuda")
+        mask = torch.rand(N, generator=g, device="cuda") < C["observed"]
+        mobs = torch.where(mask, x, torch.zeros_like(x))
+        cfg = pk.SolverConfig(phi=pk.MCP(2.5), psi=pk.MCP(2.5), randomized=True, sketch=sk,
+                              max_iters=args.steps + args.warmup, tol=1e-30)
+        cm = ColMajor(mobs, dims, "torch", None)
+        run = NativeSolver("gnhtc", cm, None, mask.to(torch.uint8), cfg, modes,
+                           cfg.lam_for(dims))
+        host_in = (mobs.reshape(dims[::-1]).permute(*reversed(range(len(dims)))).cpu().numpy(),
+                   mask.reshape(dims[::-1]).permute(*reversed(range(len(dims)))).cpu().numpy())
+    else:
+        x = x / x.abs().max()
+        m = int(C["observed"] * N)
+        idx = torch.randint(0, N, (m,), generator=g, device="cuda")
+        y = x[idx] + C["sigma"] * torch.randn(m, generator=g, device="cuda")
+        dither = (torch.rand(m, generator=g, device="cuda") * 2 - 1) * C["theta"]
+        sgn = torch.where(y + dither >= 0, 1.0, -1.0)
+        j2 = torch.bincount(idx, minlength=N).float()
+        j1 = C["theta"] * torch.bincount(idx, weights=sgn, minlength=N).float()
+        cfg = pk.SolverConfig.one_bit(phi=pk.MCP(2.5), psi=pk.MCP(2.5), randomized=True,
+                                      sketch=sk, max_iters=args.steps + args.warmup, tol=1e-30)
+        run = NativeSolver("gnobhtc", ColMajor(j1, dims, "torch", None),
+                           ColMajor(j2, dims, "torch", None), None, cfg, modes,
+                           cfg.lam_for(dims), alpha=1.0, mcount=float(m))
+        host_in = (idx.cpu().numpy(), sgn.to(torch.int8).cpu().numpy(), j1, j2, m)
+    stream = torch.cuda.ExternalStream(lib.tr_admm_stream(run.handle))
+    for _ in range(args.warmup):
+        run.step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = lib.tr_launch_count()
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            run.step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = lib.tr_launch_count() - launches0
+    ms = e0.elapsed_time(e1) / args.steps
+    lib.tr_profile_enable(1)
+    for _ in range(2):
+        run.step()
+    torch.cuda.synchronize()
+    prof = _lib.profile_read()
+    lib.tr_profile_enable(0)
+    run.close()
+    value = len(modes) * N / (ms / 1e3)
+    # end to end through the public API with host arrays
+    e2e_iters = 3
+    if C["solver"] == "gnhtc":
+        mo_h, mk_h = host_in
+        cfg_e = pk.SolverConfig(phi=pk.MCP(2.5), psi=pk.MCP(2.5), randomized=True, sketch=sk,
+                                max_iters=e2e_iters, tol=1e-30)
+        t0 = time.perf_counter()
+        l_h, rep = pk.gnhtc(mo_h, mk_h, cfg_e)
+        e2e_s = time.perf_counter() - t0
+        h2d, d2h = mo_h.nbytes + mk_h.nbytes, l_h.nbytes
+        api = f"paper_2506_09594_b200.gnhtc(numpy, max_iters={e2e_iters})"
+    else:
+        idx_h, sgn_h, j1, j2, m = host_in
+        dims_f = tuple(dims)
+        perm = tuple(reversed(range(len(dims))))
+        obs = pk.ObservationSet(dims=dims_f, theta=C["theta"], indices=idx_h, signs=sgn_h,
+                                j1=j1.reshape(dims[::-1]).permute(*perm).cpu().numpy(),
+                                j2=j2.reshape(dims[::-1]).permute(*perm).cpu().numpy())
+        cfg_e = pk.SolverConfig.one_bit(phi=pk.MCP(2.5), psi=pk.MCP(2.5), randomized=True,
+                                        sketch=sk, max_iters=e2e_iters, tol=1e-30)
+        t0 = time.perf_counter()
+        l_h, rep = pk.gnobhtc(obs, cfg_e, alpha=1.0)
+        e2e_s = time.perf_counter() - t0
+        h2d, d2h = obs.j1.nbytes + obs.j2.nbytes, np.asarray(l_h).nbytes
+        api = f"paper_2506_09594_b200.gnobhtc(ObservationSet f32, max_iters={e2e_iters})"
+    # roofline: the dominant HBM category with its algorithmic bytes
+    peak, peak_kind = peaks()
+    algo = admm_bytes(dims, 4, len(modes))
+    cats = {k: v for k, v in prof.items() if k in algo and k != "admm_rhs"}
+    dom = max(cats, key=lambda k: cats[k][0]) if cats else None
+    roof = None
+    if dom:
+        per_ms = cats[dom][0] / 2
+        ach = algo[dom] / (per_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": round(ach / peak, 4),
+                "traffic": None, "algorithmic_bytes_per_step": algo[dom],
+                "share_of_step": round(per_ms / ms, 4)}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Gaussian-factor t-product)",
+        "config": {"workload": C["workload"], "step": "admm", "dims": list(dims),
+                   "ranks": list(C["ranks"]), "blocks": list(C["blocks"]),
+                   "krylov": list(C["krylov"]), "gradient_modes": list(modes),
+                   "solver": C["solver"], "parallelism": "replicas1", "note": C["note"]},
+        "admm_iters_per_s": 1e3 / ms,
+        "e2e": {"value": len(modes) * N * rep.iterations / e2e_s, "unit": UNIT,
+                "h2d_bytes_per_step": h2d / rep.iterations, "d2h_bytes_per_step": d2h / rep.iterations,
+                "api": api},
+        "gpu_launches": launches, "roofline": roof,
+        "kernel_ms_per_step": {k: round(v[0] / 2, 4)
+                               for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])},
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 CONFIG4 = {
     "workload": "robust-completion-2048x2048x32x(4N)-f32",
     "local_dims": (2048, 2048, 32, 4),
@@ -934,6 +1090,8 @@ def main():
                     default="admm")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-legs", action="store_true", help="skip the fp64 and BLBP legs")
+    ap.add_argument("--config", type=int, default=1, choices=(1, 2, 3),
+                    help="BASELINE configs[k] of the ADMM step (1 = the bench default)")
     ap.add_argument("--lrta", choices=("bki", "blbp"), default="bki",
                     help="sketch of the ADMM step's t-SVTs: fixed-rank block Krylov (default) "
                          "or fixed-accuracy block Lanczos")
@@ -942,6 +1100,8 @@ def main():
         run_reference(args)
     elif args.step == "admm-sharded":
         run_admm_sharded(args)
+    elif args.config in CONFIGS:
+        run_config(args)
     else:
         run_ours(args)
 

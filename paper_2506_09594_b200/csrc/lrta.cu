@@ -272,27 +272,40 @@ static int64_t panel_mma_launch(const float* A, const float* P, const float* coe
 }
 
 // MODE 0 draws the sketch rows into `rows` ((n + 16) x b scratch) first.
+// Blocks wider than 8 columns run as ceil(b / 8) passes of up to 8 columns
+// each (column-separable products, see PanelMmaArgs::j0); the tensor-core pass
+// read twice still beats the CUDA-core fallback several times over.
 template <int MODE>
 static int64_t panel_mma(const float* A, int64_t m, int64_t n, int b, const float* P,
                          const float* gover, SketchSpec sk, float* rows, double* partial,
                          cudaStream_t st) {
   static const bool off = getenv("TR_NO_PANEL_MMA") != nullptr;
-  if (off || m > 1024 || b > 8 || rows == nullptr) return -1;
-  PanelMmaArgs pa;
-  pa.m = m;
-  pa.n = n;
-  pa.b = b;
-  pa.S = panel_mma_slot(m);
-  pa.nst = 2;
-  pa.nchunks = cdiv(n, kPmCols);
-  if (MODE == 0) {
-    const int64_t total = pa.nchunks * kPmCols * b;
-    launch("sketch_rows", k_sketch_rows, (unsigned)std::min<int64_t>(cdiv(total, 256), 4 * num_sms()),
-           256, 0, st, n, b, sk, gover, rows);
+  static const int max_b = getenv("TR_PANEL_MMA_MAXB") ? atoi(getenv("TR_PANEL_MMA_MAXB")) : 32;
+  if (off || m > 1024 || b > max_b || rows == nullptr) return -1;
+  int64_t np = -1;
+  for (int j0 = 0; j0 < b; j0 += 8) {
+    const int bw = std::min(8, b - j0);
+    PanelMmaArgs pa;
+    pa.m = m;
+    pa.n = n;
+    pa.b = bw;
+    pa.j0 = j0;
+    pa.b_all = b;
+    pa.S = panel_mma_slot(m);
+    pa.nst = 2;
+    pa.nchunks = cdiv(n, kPmCols);
+    if (MODE == 0) {
+      const int64_t total = pa.nchunks * kPmCols * bw;
+      launch("sketch_rows", k_sketch_rows,
+             (unsigned)std::min<int64_t>(cdiv(total, 256), 4 * num_sms()), 256, 0, st, n, bw, sk,
+             gover, rows, j0, b);
+    }
+    const float* cf = MODE == 0 ? rows : nullptr;
+    const float* Pj = MODE == 1 ? P + m * (int64_t)j0 : P;
+    np = m <= 512 ? panel_mma_launch<1, MODE>(A, Pj, cf, pa, partial, st)
+                  : panel_mma_launch<2, MODE>(A, Pj, cf, pa, partial, st);
   }
-  const float* cf = MODE == 0 ? rows : nullptr;
-  return m <= 512 ? panel_mma_launch<1, MODE>(A, P, cf, pa, partial, st)
-                  : panel_mma_launch<2, MODE>(A, P, cf, pa, partial, st);
+  return np;
 }
 
 template <int MODE>

@@ -92,6 +92,11 @@ struct PanelMmaArgs {
   int S;    // column slot stride in floats (round_up(m, 32) + 8)
   int nst;  // ring depth
   int64_t nchunks;
+  // sketch columns [j0, j0 + b) of a block of b_all: both products are
+  // column-separable (Y_j = A G_j, Y_j = A (A^T P_j)), so a block wider than
+  // the 8-column MMA tile runs as several passes writing their columns of the
+  // per-CTA partial (stride b_all * m)
+  int j0 = 0, b_all = 0;
 };
 
 // slot covers every row a compute warp touches (rows >= m stay zero), S = 8 mod 32
@@ -101,21 +106,23 @@ __host__ __device__ constexpr int panel_mma_slot(int64_t m) {
 
 // rows[c * b + j] = sketch entry (c, j) of physical column c (logical-column
 // remap, override or Philox), zero for c >= n (up to the chunk pad)
+// (columns [j0, j0 + b) of a sketch of b_all columns; rows[c * b + j])
 __global__ void k_sketch_rows(int64_t n, int b, SketchSpec sk, const float* __restrict__ gover,
-                              float* __restrict__ rows) {
+                              float* __restrict__ rows, int j0, int b_all) {
   const int64_t npad = (n + kPmCols - 1) / kPmCols * kPmCols;
   const int64_t eff = sk.inner_eff ? *sk.inner_eff : sk.inner;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < npad * b;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = e / b;
-    const int j = (int)(e % b);
+    const int j = (int)(e % b) + j0;
     float v = 0.f;
     if (c < n) {
       const int64_t col = c + sk.col0;  // global column
       const int64_t lo = col % sk.inner, f = col / sk.inner;
       if (lo < eff) {
         const int64_t cl = lo + eff * f;
-        v = gover ? gover[cl * b + j] : (float)gauss_at(sk.seed, sk.stream, (uint64_t)(cl * b + j));
+        v = gover ? gover[cl * b_all + j]
+                  : (float)gauss_at(sk.seed, sk.stream, (uint64_t)(cl * b_all + j));
       }
     }
     rows[e] = v;
@@ -370,7 +377,7 @@ __global__ void __launch_bounds__(kPmThreads, 1)
   }
 
   // y: (row r0, sketch column 2t / 2t+1), (row r0+1, ...)
-  double* out = partial + (int64_t)blockIdx.x * b * m;
+  double* out = partial + (int64_t)blockIdx.x * pa.b_all * m + (int64_t)pa.j0 * m;
 #pragma unroll
   for (int rg = 0; rg < RG; ++rg)
 #pragma unroll
