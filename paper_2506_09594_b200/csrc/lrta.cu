@@ -536,8 +536,12 @@ static int bki_mode(const Shape& sh, const T* A, int64_t m, int64_t n, int r, in
   if (allreduce(sh, bf.M, (int64_t)s * s, st)) return 1;  // W rows are sharded
   // Jacobi in one CTA; F = Z V_top and the canonical signs over many CTAs
   const bool split = s <= 32 && r <= 32 && getenv("TR_NO_RITZ_APPLY") == nullptr;
-  launch("ritz", k_ritz<T>, 1, 256, 2 * 64 * 65 * sizeof(double), st, bf.M, s, bf.Z, m, r, V,
-         split ? (double*)nullptr : F, Ft, info);
+  static const bool two_sided = getenv("TR_RITZ_2S") != nullptr;
+  if (split && !two_sided)
+    launch("ritz", k_ritz_pc, 1, 256, 0, st, (const double*)bf.M, s, r, V, info);
+  else
+    launch("ritz", k_ritz<T>, 1, 256, 2 * 64 * 65 * sizeof(double), st, bf.M, s, bf.Z, m, r, V,
+           split ? (double*)nullptr : F, Ft, info);
   if (split)
     launch("ritz", k_ritz_apply<T>, (unsigned)cdiv(m, 32), 256, 0, st, (const double*)bf.Z, m,
            s, V, r, (const int64_t*)info, F, Ft, bf.rpv, bf.rpi, bf.ticket + 1);

@@ -466,6 +466,228 @@ __global__ void __launch_bounds__(1024) k_orth(const double* __restrict__ K, int
 __device__ long long g_ritz_probe[4];
 #endif
 
+// Rayleigh-Ritz (sketch.py:261-265) for s_eff <= 32 by QR-preconditioned
+// one-sided Jacobi (Drmac-Veselic): a complete-pivoting Cholesky P M P^T =
+// R^T R, then one-sided (Hestenes) Jacobi on the columns of R^T.  The columns
+// of R^T V become orthogonal -- normalised, they are the eigenvectors of
+// P M P^T, their squared norms the eigenvalues.  The Krylov Gram matrices are
+// strongly graded (eigenvalues over many decades), for which the pivoted
+// factor is nearly orthogonal already: a few sweeps instead of the ~8 of
+// two-sided Jacobi on M.  16 threads per column pair, one barrier per round.
+// V (s x r) = the top r_eff eigenvectors (rows un-permuted), descending; signs
+// are fixed by k_ritz_apply.  A numerically rank-deficient M (pivot below
+// 1e-15 of the largest diagonal) leaves its null space to an orthonormal
+// completion -- eigenvalue-0 Ritz vectors the reference's eigh also fixes
+// arbitrarily.
+__global__ void __launch_bounds__(256) k_ritz_pc(const double* __restrict__ Mfull, int s, int r,
+                                                 double* __restrict__ V,
+                                                 int64_t* __restrict__ info) {
+  constexpr int LD = 33;
+  __shared__ double A[32 * LD], B[32 * LD];
+  __shared__ unsigned char sched[31][16][2];
+  __shared__ int perm[32], order[32];
+  __shared__ double nrm[32];
+  __shared__ int piv_s, rank_s, rot_any;
+  __shared__ double dmax_s;
+  const int n = (int)info[0];  // s_eff
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < 32 * 32; e += 256) {
+    const int i = e & 31, j = e >> 5;
+    A[i + LD * j] = (i < n && j < n) ? Mfull[i + s * j] : 0.0;
+    B[i + LD * j] = 0.0;
+  }
+  if (tid < 32) perm[tid] = tid;
+  if (tid == 0) rank_s = n;
+  __syncthreads();
+  if (warp == 0) {
+    double d = lane < n ? A[lane + LD * lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+    if (lane == 0) dmax_s = d;
+  }
+  __syncthreads();
+  const double tol = 1e-15 * dmax_s;
+#ifdef TR_RITZ_PROBE
+  const long long t_c0 = clock64();
+#endif
+  // ---- complete-pivoting Cholesky ----
+  for (int k = 0; k < n; ++k) {
+    if (warp == 0) {
+      double v = (lane >= k && lane < n) ? A[lane + LD * lane] : -1.0;
+      int idx = lane;
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+        if (ov > v || (ov == v && oi < idx)) {
+          v = ov;
+          idx = oi;
+        }
+      }
+      if (lane == 0) {
+        piv_s = idx;
+        if (!(v > tol)) rank_s = k;
+      }
+    }
+    __syncthreads();
+    if (rank_s == k) break;
+    const int p = piv_s;
+    if (p != k) {
+      // symmetric swap of rows / columns k, p of the Schur complement, rows of R^T
+      for (int i = tid; i < n; i += 256) {
+        double t = A[k + LD * i];
+        A[k + LD * i] = A[p + LD * i];
+        A[p + LD * i] = t;
+      }
+      __syncthreads();
+      for (int i = tid; i < n; i += 256) {
+        double t = A[i + LD * k];
+        A[i + LD * k] = A[i + LD * p];
+        A[i + LD * p] = t;
+      }
+      for (int j = tid; j < k; j += 256) {
+        double t = B[k + LD * j];
+        B[k + LD * j] = B[p + LD * j];
+        B[p + LD * j] = t;
+      }
+      if (tid == 0) {
+        const int t = perm[k];
+        perm[k] = perm[p];
+        perm[p] = t;
+      }
+      __syncthreads();
+    }
+    const double dk = sqrt(A[k + LD * k]);
+    for (int j = k + tid; j < n; j += 256) B[j + LD * k] = j == k ? dk : A[k + LD * j] / dk;
+    __syncthreads();
+    const int w = n - k - 1;
+    for (int e = tid; e < w * w; e += 256) {
+      const int i = k + 1 + e % w, j = k + 1 + e / w;
+      A[i + LD * j] -= B[i + LD * k] * B[j + LD * k];
+    }
+    __syncthreads();
+  }
+  const int rank = rank_s;
+#ifdef TR_RITZ_PROBE
+  const long long t_c1 = clock64();
+  int nsweeps = 0;
+#endif
+  // ---- one-sided Jacobi on the columns of R^T (n rows, rank columns) ----
+  const int ne = rank + (rank & 1);
+  const int npairs = ne / 2;
+  for (int e = tid; e < (ne - 1) * npairs; e += 256) {
+    const int rnd = e / npairs, kk = e - rnd * npairs;
+    int p = rr_player(kk, rnd, ne), q = rr_player(ne - 1 - kk, rnd, ne);
+    if (p > q) {
+      const int t = p;
+      p = q;
+      q = t;
+    }
+    sched[rnd][kk][0] = (unsigned char)p;
+    sched[rnd][kk][1] = (unsigned char)q;
+  }
+  if (tid == 0) rot_any = 0;
+  __syncthreads();
+  const int kp = tid >> 4, j = tid & 15;  // pair kp, rows j and j + 16
+  const unsigned hmask = 0xFFFFu << (tid & 16);
+  for (int sweep = 0; sweep < 40 && ne >= 2; ++sweep) {
+    for (int rnd = 0; rnd < ne - 1; ++rnd) {
+      if (kp < npairs) {
+        const int p = sched[rnd][kp][0], q = sched[rnd][kp][1];
+        if (q < rank) {
+          const double ap0 = B[j + LD * p], ap1 = B[j + 16 + LD * p];
+          const double aq0 = B[j + LD * q], aq1 = B[j + 16 + LD * q];
+          double al = ap0 * ap0 + ap1 * ap1, be = aq0 * aq0 + aq1 * aq1,
+                 ga = ap0 * aq0 + ap1 * aq1;
+#pragma unroll
+          for (int o = 8; o > 0; o >>= 1) {
+            al += __shfl_xor_sync(hmask, al, o);
+            be += __shfl_xor_sync(hmask, be, o);
+            ga += __shfl_xor_sync(hmask, ga, o);
+          }
+          if (fabs(ga) > 1e-15 * sqrt(al * be) && ga != 0.0) {
+            if (j == 0) rot_any = 1;
+            double c, sn;
+            jacobi_cs(al, be, ga, c, sn);
+            B[j + LD * p] = c * ap0 - sn * aq0;
+            B[j + 16 + LD * p] = c * ap1 - sn * aq1;
+            B[j + LD * q] = sn * ap0 + c * aq0;
+            B[j + 16 + LD * q] = sn * ap1 + c * aq1;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    const int any = rot_any;
+    __syncthreads();
+    if (tid == 0) rot_any = 0;
+    __syncthreads();
+#ifdef TR_RITZ_PROBE
+    ++nsweeps;
+#endif
+    if (!any) break;
+  }
+#ifdef TR_RITZ_PROBE
+  if (tid == 0) {
+    info[4] = t_c1 - t_c0;
+    info[5] = clock64() - t_c1;
+    info[6] = nsweeps;
+    info[7] = rank;
+  }
+#endif
+  // ---- eigenpairs: normalised columns (eigenvalue = squared norm), descending ----
+  if (tid < 32) {
+    double x = 0.0;
+    if (tid < rank)
+      for (int i = 0; i < n; ++i) x += B[i + LD * tid] * B[i + LD * tid];
+    nrm[tid] = tid < rank ? x : -1.0;
+  }
+  __syncthreads();
+  if (tid < 32) {
+    int rk = 0;
+    const double me = nrm[tid];
+    for (int c = 0; c < rank; ++c) {
+      const double o = nrm[c];
+      rk += (o > me || (o == me && c < tid)) ? 1 : 0;
+    }
+    if (tid < rank) order[rk] = tid;
+  }
+  __syncthreads();
+  // normalise the kept columns into A (rows un-permuted): A[perm[i], c] = B[i, order[c]] / norm
+  for (int e = tid; e < 32 * 32; e += 256) A[e] = 0.0;
+  __syncthreads();
+  for (int e = tid; e < n * rank; e += 256) {
+    const int i = e % n, c = e / n;
+    const int src = order[c];
+    A[perm[i] + LD * c] = B[i + LD * src] / sqrt(nrm[src]);
+  }
+  __syncthreads();
+  const int re = min(r, n);
+  // orthonormal completion beyond the numerical rank (Gram-Schmidt of unit vectors)
+  if (re > rank && warp == 0) {
+    int c = rank;
+    for (int u = 0; u < n && c < re; ++u) {
+      double x = lane == u ? 1.0 : 0.0;
+      for (int q = 0; q < c; ++q) {
+        double dot = lane < n ? A[lane + LD * q] * (lane == u ? 1.0 : 0.0) : 0.0;
+        for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        x -= dot * (lane < n ? A[lane + LD * q] : 0.0);
+      }
+      double x2 = lane < n ? x * x : 0.0;
+      for (int o = 16; o > 0; o >>= 1) x2 += __shfl_xor_sync(0xffffffffu, x2, o);
+      if (x2 > 1e-2) {
+        if (lane < n) A[lane + LD * c] = x / sqrt(x2);
+        ++c;
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < s * r; e += 256) {
+    const int row = e % s, col = e / s;
+    V[e] = (col < re && row < n) ? A[row + LD * col] : 0.0;
+  }
+  if (tid == 0) info[1] = re;
+}
+
 // Rayleigh-Ritz (sketch.py:261-265): eigenvectors of M = W^T W by parallel
 // cyclic Jacobi, descending order, F = Z V; then the canonical sign (largest
 // |entry| of every factor column positive, first index on ties).
