@@ -247,8 +247,10 @@ static int64_t panel_launch(const T* A, const T* P, const T* gover, PanelArgs pa
   return grid;
 }
 
-// Tensor-core Krylov pass (panel_mma.cuh): fp32 unfoldings with m <= 1024, b <= 8.
-template <int RG, int MODE>
+// Tensor-core Krylov pass (panel_mma.cuh): fp32 unfoldings with m <= 1024
+// (one CTA per chunk sequence) or m <= 2048 (CL = 2: a 2-CTA cluster splits
+// the rows), b <= 8 per pass.
+template <int RG, int MODE, int CL>
 static int64_t panel_mma_launch(const float* A, const float* P, const float* coef,
                                 PanelMmaArgs pa, double* partial, cudaStream_t st) {
   const size_t fixed =
@@ -258,17 +260,17 @@ static int64_t panel_mma_launch(const float* A, const float* P, const float* coe
   pa.nst = (int)std::min<size_t>(kPmMaxStages, (220 * 1024 - fixed) / stage);
   static const int nst_cap = getenv("TR_PM_STAGES") ? atoi(getenv("TR_PM_STAGES")) : 0;
   if (nst_cap >= 2) pa.nst = std::min(pa.nst, nst_cap);
-  const int64_t grid = std::min<int64_t>(pa.nchunks, stream_sms());
+  const int64_t clusters = std::min<int64_t>(pa.nchunks, stream_sms() / CL);
   const size_t smem = pa.nst * stage + fixed;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_panel_mma<RG, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_panel_mma<RG, MODE, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          220 * 1024);
     attr = true;
   }
-  launch(MODE ? "panel_gram" : "panel_sketch", k_panel_mma<RG, MODE>, (unsigned)grid, kPmThreads,
-         smem, st, A, P, coef, pa, partial);
-  return grid;
+  launch(MODE ? "panel_gram" : "panel_sketch", k_panel_mma<RG, MODE, CL>,
+         (unsigned)(clusters * CL), kPmThreads, smem, st, A, P, coef, pa, partial);
+  return clusters;
 }
 
 // MODE 0 draws the sketch rows into `rows` ((n + 16) x b scratch) first.
@@ -281,7 +283,11 @@ static int64_t panel_mma(const float* A, int64_t m, int64_t n, int b, const floa
                          cudaStream_t st) {
   static const bool off = getenv("TR_NO_PANEL_MMA") != nullptr;
   static const int max_b = getenv("TR_PANEL_MMA_MAXB") ? atoi(getenv("TR_PANEL_MMA_MAXB")) : 32;
-  if (off || m > 1024 || b > max_b || rows == nullptr) return -1;
+  // m in (1024, 2048]: the 2-CTA cluster split (TR_NO_PANEL_CLUSTER / _SKETCH: the CUDA-core pass)
+  static const bool no_cl = getenv("TR_NO_PANEL_CLUSTER") != nullptr;
+  static const bool no_cl0 = getenv("TR_NO_PANEL_CLUSTER_SKETCH") != nullptr;
+  if (off || m > ((no_cl || (MODE == 0 && no_cl0)) ? 1024 : 2048) || b > max_b || rows == nullptr)
+    return -1;
   int64_t np = -1;
   for (int j0 = 0; j0 < b; j0 += 8) {
     const int bw = std::min(8, b - j0);
@@ -291,7 +297,7 @@ static int64_t panel_mma(const float* A, int64_t m, int64_t n, int b, const floa
     pa.b = bw;
     pa.j0 = j0;
     pa.b_all = b;
-    pa.S = panel_mma_slot(m);
+    pa.S = panel_mma_slot(m > 1024 ? ((m + 1) / 2 + 3) / 4 * 4 : m);
     pa.nst = 2;
     pa.nchunks = cdiv(n, kPmCols);
     if (MODE == 0) {
@@ -302,8 +308,9 @@ static int64_t panel_mma(const float* A, int64_t m, int64_t n, int b, const floa
     }
     const float* cf = MODE == 0 ? rows : nullptr;
     const float* Pj = MODE == 1 ? P + m * (int64_t)j0 : P;
-    np = m <= 512 ? panel_mma_launch<1, MODE>(A, Pj, cf, pa, partial, st)
-                  : panel_mma_launch<2, MODE>(A, Pj, cf, pa, partial, st);
+    np = m <= 512    ? panel_mma_launch<1, MODE, 1>(A, Pj, cf, pa, partial, st)
+         : m <= 1024 ? panel_mma_launch<2, MODE, 1>(A, Pj, cf, pa, partial, st)
+                     : panel_mma_launch<2, MODE, 2>(A, Pj, cf, pa, partial, st);
   }
   return np;
 }

@@ -183,17 +183,64 @@ __device__ __forceinline__ void panel_fused(const float* __restrict__ As1,
   }
 }
 
+__device__ __forceinline__ uint32_t pm_cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+// shared::cluster address of `p` (a local shared variable) in CTA `rank`
+__device__ __forceinline__ uint32_t pm_mapa(const void* p, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(smem_u32(p)), "r"(rank));
+  return out;
+}
+
+__device__ __forceinline__ void pm_st_cluster(uint32_t addr, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+
+__device__ __forceinline__ void pm_arrive_remote(uint32_t bar_cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                   bar_cluster_addr)
+               : "memory");
+}
+
+__device__ __forceinline__ void pm_wait_cluster(uint64_t* bar, uint32_t phase) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+}
+
 // RG = 32-row groups per compute warp (m <= 512 RG); b <= 8.
 // MODE 0: `coef` = k_sketch_rows output; MODE 1: P (m x b column-major).
-template <int RG, int MODE>
-__global__ void __launch_bounds__(kPmThreads, 1)
+// CL = 2: the rows are split over a 2-CTA cluster (m <= 2048; each CTA streams
+// its half of every column chunk); in the gram mode the two halves of each
+// chunk's T partial are exchanged through distributed shared memory and
+// summed in CTA order on both sides, so T -- and Y -- are bit-identical to a
+// single CTA's fixed-order sum of the same warps.
+template <int RG, int MODE, int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kPmThreads, 1)
     k_panel_mma(const float* __restrict__ A, const float* __restrict__ P,
                 const float* __restrict__ coef, PanelMmaArgs pa, double* __restrict__ partial) {
   extern __shared__ __align__(128) unsigned char pm_smem[];
   __shared__ __align__(8) uint64_t full[kPmMaxStages], empty[kPmMaxStages];
   __shared__ __align__(8) uint64_t redfull[2], redempty[2], tready[2], tempty[2];
+  __shared__ __align__(8) uint64_t xfull[2], xempty[2];  // CL = 2: the peer's T partial
+  __shared__ float xbuf[2][kPmTE];
+  const uint32_t crank = CL > 1 ? pm_cluster_rank() : 0u;
   const int S = pa.S;
-  const int64_t m = pa.m;
+  const int64_t mfull = pa.m;  // rows of A, P, Y
+  // this CTA's rows [mrow0, mrow0 + m): the first half rounded to 4 (16-byte copies)
+  const int64_t mh = CL > 1 ? ((pa.m + 1) / 2 + 3) / 4 * 4 : pa.m;
+  const int64_t mrow0 = crank == 0 ? 0 : mh;
+  const int64_t m = crank == 0 ? mh : pa.m - mh;
   const int b = pa.b;
   const int nst = pa.nst;
   const size_t stage_elems = (size_t)kPmCols * S;
@@ -204,9 +251,9 @@ __global__ void __launch_bounds__(kPmThreads, 1)
   float* tlo = thi + 2 * kPmTE;             // MODE 1: 2 x kPmTE
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int64_t G = gridDim.x;
-  const int64_t my_chunks =
-      pa.nchunks > (int64_t)blockIdx.x ? (pa.nchunks - 1 - blockIdx.x) / G + 1 : 0;
+  const int64_t G = gridDim.x / CL;        // clusters (one chunk sequence each)
+  const int64_t cid = blockIdx.x / CL;
+  const int64_t my_chunks = pa.nchunks > cid ? (pa.nchunks - 1 - cid) / G + 1 : 0;
 
   // zeroed ring: padding rows and the absent columns of a partial chunk stay finite
   {
@@ -225,18 +272,26 @@ __global__ void __launch_bounds__(kPmThreads, 1)
       mbar_init(&redempty[k], 32);
       mbar_init(&tready[k], 32);
       mbar_init(&tempty[k], kPmWarps * 32);
+      mbar_init(&xfull[k], 32);
+      mbar_init(&xempty[k], 32);
     }
     fence_barrier_init();
   }
-  __syncthreads();
+  if (CL > 1) {
+    // every CTA's barriers exist before the peer's first remote arrive
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                     : "memory");
+  } else {
+    __syncthreads();
+  }
 
   if (warp == kPmWarps + 1) {  // ---- producer (one thread; no divisions in the loop) ----
     if (lane == 0) {
       const uint32_t bytes = (uint32_t)(m * sizeof(float));
       const uint32_t cbytes = (uint32_t)(kPmCols * b * sizeof(float));
       const int64_t cstep = G * kPmCols;
-      int64_t c0 = (int64_t)blockIdx.x * kPmCols;
-      const float* src = A + c0 * m;
+      int64_t c0 = cid * kPmCols;
+      const float* src = A + c0 * mfull + mrow0;
       int s = 0;
       uint32_t ph = 0;
       for (int64_t it = 0; it < my_chunks; ++it) {
@@ -246,148 +301,173 @@ __global__ void __launch_bounds__(kPmThreads, 1)
         float* dst = stages + s * stage_elems;
         if (cols == kPmCols) {
 #pragma unroll
-          for (int c = 0; c < kPmCols; ++c) bulk_g2s(dst + c * S, src + c * m, bytes, &full[s]);
+          for (int c = 0; c < kPmCols; ++c) bulk_g2s(dst + c * S, src + c * mfull, bytes, &full[s]);
         } else {
-          for (int c = 0; c < cols; ++c) bulk_g2s(dst + c * S, src + c * m, bytes, &full[s]);
+          for (int c = 0; c < cols; ++c) bulk_g2s(dst + c * S, src + c * mfull, bytes, &full[s]);
         }
         if (MODE == 0) bulk_g2s(cst + s * kPmCols * b, coef + c0 * b, cbytes, &full[s]);
         c0 += cstep;
-        src += cstep * m;
+        src += cstep * mfull;
         if (++s == nst) {
           s = 0;
           ph ^= 1u;
         }
       }
     }
-    return;
-  }
-  if (warp == kPmWarps) {  // ---- reducer (gram) ----
+  } else if (warp == kPmWarps) {  // ---- reducer (gram) ----
     if (MODE == 1) {
+      const uint32_t peer = crank ^ 1u;
       for (int64_t it = 0; it < my_chunks; ++it) {
         const int k = (int)(it & 1);
         const uint32_t ph = (uint32_t)((it >> 1) & 1);
-        const int64_t c0 = (blockIdx.x + it * G) * kPmCols;
+        const int64_t c0 = (cid + it * G) * kPmCols;
         const int cols = (int)((pa.n - c0) < kPmCols ? (pa.n - c0) : kPmCols);
         mbar_wait(&redfull[k], ph);
         mbar_wait(&tempty[k], ph ^ 1);
         const float* rk = red + k * kPmWarps * kPmRS;
+        float v[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int e = lane + 32 * h;  // e = j * 8 + column
-          float v = 0.f;
+          float x = 0.f;
 #pragma unroll
-          for (int w = 0; w < kPmWarps; ++w) v += rk[w * kPmRS + e];
-          if ((e & 7) >= cols || (e >> 3) >= b) v = 0.f;
-          const uint32_t hv = f2tf32(v);
+          for (int w = 0; w < kPmWarps; ++w) x += rk[w * kPmRS + e];
+          v[h] = x;
+        }
+        if (CL > 1) {
+          // this half's partial -> the peer's xbuf[k]; the peer's -> ours; sum in CTA order
+          pm_wait_cluster(&xempty[k], ph ^ 1);  // the peer has consumed its xbuf[k]
+#pragma unroll
+          for (int h = 0; h < 2; ++h) pm_st_cluster(pm_mapa(&xbuf[k][lane + 32 * h], peer), v[h]);
+          pm_arrive_remote(pm_mapa(&xfull[k], peer));
+          pm_wait_cluster(&xfull[k], ph);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const float o = xbuf[k][lane + 32 * h];
+            v[h] = crank == 0 ? v[h] + o : o + v[h];
+          }
+          pm_arrive_remote(pm_mapa(&xempty[k], peer));  // our xbuf[k] may be refilled
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int e = lane + 32 * h;
+          float x = v[h];
+          if ((e & 7) >= cols || (e >> 3) >= b) x = 0.f;
+          const uint32_t hv = f2tf32(x);
           thi[k * kPmTE + e] = __uint_as_float(hv);
-          tlo[k * kPmTE + e] = v - __uint_as_float(hv);
+          tlo[k * kPmTE + e] = x - __uint_as_float(hv);
         }
         mbar_arrive(&redempty[k]);
         mbar_arrive(&tready[k]);
       }
     }
-    return;
-  }
+  } else {
+    // ---- compute warps ----
+    // step-1 A operand = [P_hi; P_lo]^T: a0 / a2 = P_hi (sketch column g) at rows
+    // 2t / 2t+1 of the 8-row step, a1 / a3 = P_lo
+    uint32_t pf[RG][4][4];
+#pragma unroll
+    for (int rg = 0; rg < RG; ++rg)
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t r = 32 * (warp * RG + rg) + 8 * ks + 2 * t + h;
+          const float p = (MODE == 1 && r < m && g < b) ? P[mrow0 + r + mfull * g] : 0.f;
+          split_tf32(p, pf[rg][ks][2 * h], pf[rg][ks][2 * h + 1]);
+        }
+    float y[RG][2][4];
+#pragma unroll
+    for (int rg = 0; rg < RG; ++rg)
+#pragma unroll
+      for (int tl = 0; tl < 2; ++tl)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) y[rg][tl][i] = 0.f;
+    const int rw0 = 32 * RG * warp;  // first row of this warp (rows >= m read zero padding)
 
-  // ---- compute warps ----
-  // step-1 A operand = [P_hi; P_lo]^T: a0 / a2 = P_hi (sketch column g) at rows
-  // 2t / 2t+1 of the 8-row step, a1 / a3 = P_lo
-  uint32_t pf[RG][4][4];
+    // stage / phase of chunk `it` and of chunk it-2 (step 2 lags two chunks)
+    int s_cur = 0, s_old = 0;
+    uint32_t ph_cur = 0;
+    const uint32_t zero2[2] = {0u, 0u};
+    for (int64_t it = 0; it < my_chunks + (MODE == 1 ? 2 : 0); ++it) {
+      const bool has1 = it < my_chunks;        // chunk it: step 1 (gram) / step 2 (sketch)
+      const bool has2 = MODE == 1 && it >= 2;  // chunk it-2: step 2 (gram)
+      const int kb = (int)(it & 1);
+      if (has1) mbar_wait(&full[s_cur], ph_cur);
+      const float* As1 = stages + s_cur * stage_elems;
+      uint32_t bh[2], bl[2];
+      if (MODE == 1) {
+        if (has2) {
+          mbar_wait(&tready[kb], (uint32_t)(((it - 2) >> 1) & 1));
+          const int e0 = g * 8 + t;  // T[column t][sketch column g]
+          bh[0] = __float_as_uint(thi[kb * kPmTE + e0]);
+          bh[1] = __float_as_uint(thi[kb * kPmTE + e0 + 4]);
+          bl[0] = __float_as_uint(tlo[kb * kPmTE + e0]);
+          bl[1] = __float_as_uint(tlo[kb * kPmTE + e0 + 4]);
+          mbar_arrive(&tempty[kb]);
+        }
+        float d[4][4];
 #pragma unroll
-  for (int rg = 0; rg < RG; ++rg)
+        for (int u = 0; u < 4; ++u)
 #pragma unroll
-    for (int ks = 0; ks < 4; ++ks)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t r = 32 * (warp * RG + rg) + 8 * ks + 2 * t + h;
-        const float p = (MODE == 1 && r < m && g < b) ? P[r + m * g] : 0.f;
-        split_tf32(p, pf[rg][ks][2 * h], pf[rg][ks][2 * h + 1]);
-      }
-  float y[RG][2][4];
-#pragma unroll
-  for (int rg = 0; rg < RG; ++rg)
-#pragma unroll
-    for (int tl = 0; tl < 2; ++tl)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) y[rg][tl][i] = 0.f;
-  const int rw0 = 32 * RG * warp;  // first row of this warp (rows >= m read zero padding)
-
-  // stage / phase of chunk `it` and of chunk it-2 (step 2 lags two chunks)
-  int s_cur = 0, s_old = 0;
-  uint32_t ph_cur = 0;
-  const uint32_t zero2[2] = {0u, 0u};
-  for (int64_t it = 0; it < my_chunks + (MODE == 1 ? 2 : 0); ++it) {
-    const bool has1 = it < my_chunks;               // chunk it: step 1 (gram) / step 2 (sketch)
-    const bool has2 = MODE == 1 && it >= 2;         // chunk it-2: step 2 (gram)
-    const int kb = (int)(it & 1);
-    if (has1) mbar_wait(&full[s_cur], ph_cur);
-    const float* As1 = stages + s_cur * stage_elems;
-    uint32_t bh[2], bl[2];
-    if (MODE == 1) {
-      if (has2) {
-        mbar_wait(&tready[kb], (uint32_t)(((it - 2) >> 1) & 1));
-        const int e0 = g * 8 + t;  // T[column t][sketch column g]
-        bh[0] = __float_as_uint(thi[kb * kPmTE + e0]);
-        bh[1] = __float_as_uint(thi[kb * kPmTE + e0 + 4]);
-        bl[0] = __float_as_uint(tlo[kb * kPmTE + e0]);
-        bl[1] = __float_as_uint(tlo[kb * kPmTE + e0 + 4]);
-        mbar_arrive(&tempty[kb]);
-      }
-      float d[4][4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) d[u][i] = 0.f;
-      const float* As2 = stages + s_old * stage_elems;
-      if (has1 && has2)
-        panel_fused<RG, true, true>(As1, As2, S, rw0, g, t, pf, d, y, bh, bl);
-      else if (has1)
-        panel_fused<RG, true, false>(As1, As2, S, rw0, g, t, pf, d, y, zero2, zero2);
-      else
-        panel_fused<RG, false, true>(As1, As2, S, rw0, g, t, pf, d, y, bh, bl);
-      if (has2) {
-        mbar_arrive(&empty[s_old]);
-        s_old = s_old + 1 == nst ? 0 : s_old + 1;
+          for (int i = 0; i < 4; ++i) d[u][i] = 0.f;
+        const float* As2 = stages + s_old * stage_elems;
+        if (has1 && has2)
+          panel_fused<RG, true, true>(As1, As2, S, rw0, g, t, pf, d, y, bh, bl);
+        else if (has1)
+          panel_fused<RG, true, false>(As1, As2, S, rw0, g, t, pf, d, y, zero2, zero2);
+        else
+          panel_fused<RG, false, true>(As1, As2, S, rw0, g, t, pf, d, y, bh, bl);
+        if (has2) {
+          mbar_arrive(&empty[s_old]);
+          s_old = s_old + 1 == nst ? 0 : s_old + 1;
+        }
+        if (has1) {
+          // d[0..1] rows g (P_hi), d[2..3] rows g+8 (P_lo): T partial (sketch column g, columns 2t / 2t+1)
+          mbar_wait(&redempty[kb], (uint32_t)(((it >> 1) & 1) ^ 1));
+          float* rw = red + (kb * kPmWarps + warp) * kPmRS;
+          *reinterpret_cast<float2*>(rw + g * 8 + 2 * t) =
+              make_float2(((d[0][0] + d[1][0]) + (d[2][0] + d[3][0])) +
+                              ((d[0][2] + d[1][2]) + (d[2][2] + d[3][2])),
+                          ((d[0][1] + d[1][1]) + (d[2][1] + d[3][1])) +
+                              ((d[0][3] + d[1][3]) + (d[2][3] + d[3][3])));
+          mbar_arrive(&redfull[kb]);
+        }
+      } else {
+        const float* cr = cst + s_cur * kPmCols * b;
+        const float v0 = g < b ? cr[t * b + g] : 0.f;
+        const float v1 = g < b ? cr[(t + 4) * b + g] : 0.f;
+        split_tf32(v0, bh[0], bl[0]);
+        split_tf32(v1, bh[1], bl[1]);
+        float d[4][4];
+        panel_fused<RG, false, true>(As1, As1, S, rw0, g, t, pf, d, y, bh, bl);
+        mbar_arrive(&empty[s_cur]);
       }
       if (has1) {
-        // d[0..1] rows g (P_hi), d[2..3] rows g+8 (P_lo): T partial (sketch column g, columns 2t / 2t+1)
-        mbar_wait(&redempty[kb], (uint32_t)(((it >> 1) & 1) ^ 1));
-        float* rw = red + (kb * kPmWarps + warp) * kPmRS;
-        *reinterpret_cast<float2*>(rw + g * 8 + 2 * t) =
-            make_float2(((d[0][0] + d[1][0]) + (d[2][0] + d[3][0])) +
-                            ((d[0][2] + d[1][2]) + (d[2][2] + d[3][2])),
-                        ((d[0][1] + d[1][1]) + (d[2][1] + d[3][1])) +
-                            ((d[0][3] + d[1][3]) + (d[2][3] + d[3][3])));
-        mbar_arrive(&redfull[kb]);
+        s_cur = s_cur + 1 == nst ? 0 : s_cur + 1;
+        ph_cur ^= s_cur == 0 ? 1u : 0u;
       }
-    } else {
-      const float* cr = cst + s_cur * kPmCols * b;
-      const float v0 = g < b ? cr[t * b + g] : 0.f;
-      const float v1 = g < b ? cr[(t + 4) * b + g] : 0.f;
-      split_tf32(v0, bh[0], bl[0]);
-      split_tf32(v1, bh[1], bl[1]);
-      float d[4][4];
-      panel_fused<RG, false, true>(As1, As1, S, rw0, g, t, pf, d, y, bh, bl);
-      mbar_arrive(&empty[s_cur]);
     }
-    if (has1) {
-      s_cur = s_cur + 1 == nst ? 0 : s_cur + 1;
-      ph_cur ^= s_cur == 0 ? 1u : 0u;
-    }
-  }
 
-  // y: (row r0, sketch column 2t / 2t+1), (row r0+1, ...)
-  double* out = partial + (int64_t)blockIdx.x * pa.b_all * m + (int64_t)pa.j0 * m;
+    // y: (row r0, sketch column 2t / 2t+1), (row r0+1, ...); the partial of a
+    // cluster covers all mfull rows (each CTA its own)
+    double* out = partial + cid * pa.b_all * mfull + (int64_t)pa.j0 * mfull + mrow0;
 #pragma unroll
-  for (int rg = 0; rg < RG; ++rg)
+    for (int rg = 0; rg < RG; ++rg)
 #pragma unroll
-    for (int tl = 0; tl < 2; ++tl)
+      for (int tl = 0; tl < 2; ++tl)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int64_t row = 32 * (warp * RG + rg) + 16 * tl + 2 * g + (i >> 1);
-        const int j = 2 * t + (i & 1);
-        if (row < m && j < b) out[(int64_t)j * m + row] = (double)y[rg][tl][i];
-      }
+        for (int i = 0; i < 4; ++i) {
+          const int64_t row = 32 * (warp * RG + rg) + 16 * tl + 2 * g + (i >> 1);
+          const int j = 2 * t + (i & 1);
+          if (row < m && j < b) out[(int64_t)j * mfull + row] = (double)y[rg][tl][i];
+        }
+  }
+  if (CL > 1) {
+    // no CTA leaves while its peer may still arrive on its barriers
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                     : "memory");
+  }
 }
 
 }  // namespace tr
