@@ -153,10 +153,32 @@ __device__ __forceinline__ void for_each_chunk(const Geom& g, F&& f) {
   LineCo lc;
   if (cpl >= (int)blockDim.x) {
     const int64_t wl = g.walk_last, per = wl > 1 ? lines / wl : lines;
+    // walk position v = vr + wl * vq visits line vr * per + vq (last axis fastest);
+    // (vr, vq) advance incrementally: no 64-bit division per line
+    const int64_t dq = wl > 1 ? (int64_t)gridDim.x / wl : 0, dr = wl > 1 ? (int64_t)gridDim.x % wl : 0;
+    int64_t vq = wl > 1 ? (int64_t)blockIdx.x / wl : 0, vr = wl > 1 ? (int64_t)blockIdx.x % wl : 0;
     for (int64_t v = blockIdx.x; v < lines; v += gridDim.x) {
-      const int64_t line = wl > 1 ? (v % wl) * per + v / wl : v;
-      lc.line = line;
-      for (int a = 1; a < g.d; ++a) lc.co[a] = (int)line_coord(g, line, a);
+      lc.line = wl > 1 ? vr * per + vq : v;
+      if (wl > 1 && lines < (1ll << 31)) {
+        // coordinates straight from the walk position: the last axis is vr, the
+        // inner axes unflatten vq (no division at all for an order-3 tensor)
+        lc.co[g.d - 1] = (int)vr;
+        uint32_t rem = (uint32_t)vq;
+        for (int a = 1; a < g.d - 2; ++a) {
+          const uint32_t n = (uint32_t)g.dims[a], q = rem / n;
+          lc.co[a] = (int)(rem - q * n);
+          rem = q;
+        }
+        if (g.d >= 3) lc.co[g.d - 2] = (int)rem;
+      } else {
+        for (int a = 1; a < g.d; ++a) lc.co[a] = (int)line_coord(g, lc.line, a);
+      }
+      vq += dq;
+      vr += dr;
+      if (vr >= wl) {
+        vr -= wl;
+        ++vq;
+      }
       for (int c = threadIdx.x; c < cpl; c += blockDim.x) f(lc, (int64_t)c * V);
     }
   } else {
@@ -510,14 +532,14 @@ __global__ void __launch_bounds__(kRedThreads) k_noise_dual(Geom g, const T* __r
 // NOISE = false: E' and Y' were already written in place by k_noise_dual
 // (launched on the main stream while the per-mode t-SVTs ran); the pass reads
 // them instead of recomputing them and leaves the 7 noise partials at zero.
-template <typename T, int KIND, int STRUCT, bool NOISE = true>
-__global__ void __launch_bounds__(kRedThreads, 1) k_sweep_tail(
+template <typename T, int KIND, int STRUCT, bool NOISE = true, int V = 4, int MINB = 1>
+__global__ void __launch_bounds__(kRedThreads, MINB) k_sweep_tail(
     Geom g, const T* __restrict__ mobs, const uint8_t* __restrict__ mask, const T* __restrict__ l,
     const T* __restrict__ lold, T* __restrict__ e, T* __restrict__ y, ModePtrs<T> gn, ModePtrs<T> go,
     ModePtrs<T> lag, ModePtrs<T> lagw, double mu, double mu_next, double p0, double p1,
     double level, const double* __restrict__ scale, T* __restrict__ rhs,
     double* __restrict__ part) {
-  constexpr int V = 4, MM = 4;  // mode slots
+  constexpr int MM = 4;  // mode slots
   __shared__ double red[32];
   // per-thread partials in T (sums over a few hundred elements), per-block fp64
   T vl[5 * MM], vn[7];
@@ -556,6 +578,9 @@ __global__ void __launch_bounds__(kRedThreads, 1) k_sweep_tail(
         } else {
           int64_t pv, nx;
           axis_offsets(g, a, lc.co[a], pv, nx);
+#ifdef TR_TAIL_PROBE_SKIP_AXIS
+          if (a >= TR_TAIL_PROBE_SKIP_AXIS) pv = nx = 0;
+#endif
           lnx[k] = ldv_nc<T, V>(l + i + nx);
           lpv[k] = ldv_nc<T, V>(l + i + pv);
           gpv[k] = ldv_nc<T, V>(gn.p[k] + i + pv);

@@ -105,6 +105,19 @@ __global__ void k_twiddles(int n, cpx<T>* __restrict__ tw) {
   tw[k] = {(T)c, (T)s};
 }
 
+// q = a / b, r = a % b with a 32-bit division when both fit (a 64-bit division is
+// ~100 instructions per thread -- a sizeable share of a register-FFT tile)
+__device__ __forceinline__ void divmod_fast(int64_t a, int64_t b, int64_t& q, int64_t& r) {
+  if (((a | b) >> 31) == 0) {
+    const uint32_t qq = (uint32_t)a / (uint32_t)b;
+    q = qq;
+    r = (uint32_t)a - qq * (uint32_t)b;
+  } else {
+    q = a / b;
+    r = a - q * b;
+  }
+}
+
 struct SolveSpec {
   int active;           // last-axis pass of the diagonal solve
   int d;                // tensor order
@@ -224,9 +237,10 @@ __global__ void __launch_bounds__(256, MINB) k_fft4(cpx<T>* __restrict__ data, i
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t line = tile * G + g;
     const bool ok = line < nlines;
-    int64_t base, es;
+    int64_t base, es, lo = 0;
     if (STRIDED) {
-      const int64_t lo = line % st, h = line / st;
+      int64_t h;
+      divmod_fast(line, st, h, lo);
       base = lo + st * (int64_t)N * h;
       es = st;
     } else {
@@ -244,10 +258,10 @@ __global__ void __launch_bounds__(256, MINB) k_fft4(cpx<T>* __restrict__ data, i
     } else {
       if (p == 0) {
         double dsum = 1.0;
-        int64_t rem = ss.lo_base + (STRIDED ? line % st : 0);
+        int64_t rem = ss.lo_base + lo;
         for (int a = 0; a < ss.d - 1; ++a) {
-          const int64_t j = rem % ss.dims[a];
-          rem /= ss.dims[a];
+          int64_t j;
+          divmod_fast(rem, ss.dims[a], rem, j);
           if (ss.lam_off[a] >= 0) dsum += lam[ss.lam_off[a] + j];
         }
         den[g] = dsum;
@@ -333,7 +347,9 @@ __global__ void __launch_bounds__(256, MINB) k_fft4_real(const void* in, void* o
       const int gl = tid % G;
       const int64_t ln = line0 + gl;
       if (ln < lines) {
-        const int64_t lb = (ln % tr_n1) + tr_n1 * (int64_t)NB * (ln / tr_n1);
+        int64_t lq, lr;
+        divmod_fast(ln, tr_n1, lq, lr);
+        const int64_t lb = lr + tr_n1 * (int64_t)NB * lq;
         for (int k = tid / G; k <= N / 2; k += P) {
           const cpx<T> a = xch[gl * LS + k];
           const cpx<T> bb = cconjt(xch[gl * LS + ((N - k) & (N - 1))]);
@@ -351,7 +367,9 @@ __global__ void __launch_bounds__(256, MINB) k_fft4_real(const void* in, void* o
       const int gl = tid % G;
       const int64_t ln = line0 + gl;
       if (ln < lines) {
-        const int64_t lb = (ln % tr_n1) + tr_n1 * (int64_t)NB * (ln / tr_n1);
+        int64_t lq, lr;
+        divmod_fast(ln, tr_n1, lq, lr);
+        const int64_t lb = lr + tr_n1 * (int64_t)NB * lq;
         constexpr int IT = (NB + P - 1) / P;
         cpx<T> st[IT];  // all loads in flight before the shared-memory stores
 #pragma unroll

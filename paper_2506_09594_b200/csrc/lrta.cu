@@ -590,6 +590,32 @@ static int lrta_compress(const T* a, const Shape& sh, uint64_t seed, const T* g0
   return 0;
 }
 
+// One transform-mode product of the core (core_svt.cuh): the staged kernel
+// (both operands in shared memory) when they fit and the grid dimensions allow
+// it, else the direct kernel.
+static void mode_product(const void* in, int in_real, void* out, int out_real, int64_t st_lo, int n,
+                         int64_t hi, const cplx* U, int inverse, double alpha, int64_t face,
+                         const Trailing& skip, unsigned g_direct, cudaStream_t st) {
+  static const bool direct = getenv("TR_MODE_PRODUCT_DIRECT") != nullptr;
+  constexpr size_t kMaxSmem = 96 * 1024;  // two CTAs per SM
+  const int64_t tiles = cdiv(st_lo, kMpTL);
+  const size_t smem = mode_product_smem(n);
+  if (direct || smem > kMaxSmem || hi > 65535 || tiles >= (1ll << 31) || cdiv(n, kMpKB) > 65535) {
+    launch("mode_product", k_mode_product, g_direct, 256, 0, st, in, in_real, out, out_real, st_lo,
+           n, hi, U, inverse, alpha, face, skip);
+    return;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_mode_product_t, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kMaxSmem);
+    attr = true;
+  }
+  launch("mode_product", k_mode_product_t,
+         dim3((unsigned)tiles, (unsigned)hi, (unsigned)cdiv(n, kMpKB)), kMpTL * kMpKB, smem, st, in,
+         in_real, out, out_real, st_lo, n, hi, U, inverse, alpha, face, skip);
+}
+
 // Transform-domain SVT of the r0 x r1 x trailing core in place (bf.core).
 template <typename T>
 static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* alphas,
@@ -627,8 +653,8 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
   for (int i = 0; i < nt; ++i) {
     const int n = (int)sh.tr.d[i];
     const int64_t hi = nfa / (st_lo / face) / n;
-    launch("mode_product", k_mode_product, g, 256, 0, st, src, src_real, bufs[cur], 0, st_lo, n,
-           hi, U[i], 0, 1.0, face, i == nt - 1 ? fwd_skip : no_skip);
+    mode_product(src, src_real, bufs[cur], 0, st_lo, n, hi, U[i], 0, 1.0, face,
+                 i == nt - 1 ? fwd_skip : no_skip, g, st);
     src = bufs[cur];
     src_real = 0;
     cur ^= 1;
@@ -650,6 +676,17 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
     // X in the free mode-product buffer
     launch("face_svt", k_face_svt_g, (unsigned)nfa, 1024, (size_t)sh.r1 * sizeof(double), st,
            faces, bufs[cur], bf.fv, (int)sh.r0, (int)sh.r1, pen, tau, mirror_tr);
+  } else if (sh.r0 <= 32 && sh.r1 <= 32 && getenv("TR_FACE_SVT_V") == nullptr) {
+    // Tucker-core faces: 8 lanes per Jacobi pair, no V accumulation (core_svt.cuh)
+    const size_t smem8 = (size_t)(2 * face + sh.r1 * sh.r1) * sizeof(cplx);
+    static bool attr8 = false;
+    if (!attr8) {
+      TR_CUDA(cudaFuncSetAttribute(k_face_svt8<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   3 * 32 * 32 * (int)sizeof(cplx)));
+      attr8 = true;
+    }
+    launch("face_svt", k_face_svt8<8>, (unsigned)nfa, 128, smem8, st, faces, (int)sh.r0,
+           (int)sh.r1, pen, tau, mirror_tr);
   } else {
     // one warp per Jacobi pair: no idle warps at the per-round barrier
     static const int fth_env = getenv("TR_FACE_THREADS") ? atoi(getenv("TR_FACE_THREADS")) : 0;
@@ -666,8 +703,7 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
     const int64_t hi = nfa / (st_lo / face) / n;
     const bool last = (i == 0);
     void* dst = last ? (void*)bf.core : (void*)bufs[cur];
-    launch("mode_product", k_mode_product, g, 256, 0, st, src, 0, dst, last ? 1 : 0, st_lo, n,
-           hi, U[i], 1, al[i], face, no_skip);
+    mode_product(src, 0, dst, last ? 1 : 0, st_lo, n, hi, U[i], 1, al[i], face, no_skip, g, st);
     src = dst;
     cur ^= 1;
   }

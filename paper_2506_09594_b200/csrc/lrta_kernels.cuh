@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(256) k_ritz_pc(const double* __restrict__ Mful
   __shared__ unsigned char sched[31][16][2];
   __shared__ int perm[32], order[32];
   __shared__ double nrm[32];
-  __shared__ int piv_s, rank_s, rot_any;
+  __shared__ int piv_s, rank_s;
   __shared__ double dmax_s;
   const int n = (int)info[0];  // s_eff
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -584,42 +584,70 @@ __global__ void __launch_bounds__(256) k_ritz_pc(const double* __restrict__ Mful
     sched[rnd][kk][0] = (unsigned char)p;
     sched[rnd][kk][1] = (unsigned char)q;
   }
-  if (tid == 0) rot_any = 0;
   __syncthreads();
   const int kp = tid >> 4, j = tid & 15;  // pair kp, rows j and j + 16
-  const unsigned hmask = 0xFFFFu << (tid & 16);
+  // next round's pair is fetched before the barrier (off the round's serial chain)
+  int pn = 0, qn = rank;
+  if (kp < npairs && ne >= 2) {
+    pn = sched[0][kp][0];
+    qn = sched[0][kp][1];
+  }
   for (int sweep = 0; sweep < 40 && ne >= 2; ++sweep) {
+    int big = 0;  // a pair of this sweep met |cos| > 1e-8
     for (int rnd = 0; rnd < ne - 1; ++rnd) {
+      const int p = pn, q = qn;
+      const bool live = q < rank;  // uniform over the pair's 16 lanes; idle slots carry zeros
       if (kp < npairs) {
-        const int p = sched[rnd][kp][0], q = sched[rnd][kp][1];
-        if (q < rank) {
-          const double ap0 = B[j + LD * p], ap1 = B[j + 16 + LD * p];
-          const double aq0 = B[j + LD * q], aq1 = B[j + 16 + LD * q];
-          double al = ap0 * ap0 + ap1 * ap1, be = aq0 * aq0 + aq1 * aq1,
-                 ga = ap0 * aq0 + ap1 * aq1;
-#pragma unroll
-          for (int o = 8; o > 0; o >>= 1) {
-            al += __shfl_xor_sync(hmask, al, o);
-            be += __shfl_xor_sync(hmask, be, o);
-            ga += __shfl_xor_sync(hmask, ga, o);
-          }
-          if (fabs(ga) > 1e-15 * sqrt(al * be) && ga != 0.0) {
-            if (j == 0) rot_any = 1;
-            double c, sn;
-            jacobi_cs(al, be, ga, c, sn);
-            B[j + LD * p] = c * ap0 - sn * aq0;
-            B[j + 16 + LD * p] = c * ap1 - sn * aq1;
-            B[j + LD * q] = sn * ap0 + c * aq0;
-            B[j + 16 + LD * q] = sn * ap1 + c * aq1;
-          }
-        }
+        const int nr = rnd + 1 < ne - 1 ? rnd + 1 : 0;
+        pn = sched[nr][kp][0];
+        qn = sched[nr][kp][1];
       }
-      __syncthreads();
+      const double ap0 = live ? B[j + LD * p] : 0.0, ap1 = live ? B[j + 16 + LD * p] : 0.0;
+      const double aq0 = live ? B[j + LD * q] : 0.0, aq1 = live ? B[j + 16 + LD * q] : 0.0;
+      double al = fma(ap0, ap0, ap1 * ap1), be = fma(aq0, aq0, aq1 * aq1),
+             ga = fma(ap0, aq0, ap1 * aq1);
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) {
+        al += __shfl_xor_sync(0xffffffffu, al, o);
+        be += __shfl_xor_sync(0xffffffffu, be, o);
+        ga += __shfl_xor_sync(0xffffffffu, ga, o);
+      }
+      const double g2 = ga * ga, ab = al * be;
+      if (g2 > 1e-30 * ab) {  // |cos| > 1e-15 (false for idle slots and zero columns)
+        big |= g2 > 1e-16 * ab;
+        // Tangent in fp32 from MUFU rsqrt / rcp on the pair scaled by a power of
+        // two to max(alpha, beta) in [1, 2) (no range guards; |gamma| <= the
+        // scaled geometric mean, and a rotating pair keeps z and gamma far from
+        // fp32 underflow together): t = sign(z) gamma / (|z| + sqrt(z^2 + gamma^2)),
+        // z = (beta - alpha) / 2.  c = (1 + t^2)^{-1/2} is completed in fp64 from
+        // the t actually used: the rotation is orthogonal to fp64 rounding, only
+        // the annihilation is fp32-accurate (the next sweep absorbs it).
+        const double sc = __hiloint2double(0x7fe00000 - (__double2hiint(fmax(al, be)) & 0x7ff00000), 0);
+        const float zf = (float)(0.5 * (be - al) * sc), gf = (float)(ga * sc);
+        const float hf = fmaf(zf, zf, gf * gf);
+        float rs, invd, cs;
+        asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(hf));
+        const float df = fabsf(zf) + hf * rs;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(invd) : "f"(df));
+        const float tf = gf * copysignf(invd, zf);
+        asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(cs) : "f"(fmaf(tf, tf, 1.0f)));
+        const double t = (double)tf;
+        const double x1 = fma(t, t, 1.0);  // in [1, 2]
+        const double c0 = (double)cs;
+        const double er = fma(-x1, c0 * c0, 1.0);  // one cubic step: seed error ~2^-21
+        const double c = fma(c0 * er, fma(0.375, er, 0.5), c0);
+        const double sn = c * t;
+        B[j + LD * p] = fma(c, ap0, -sn * aq0);
+        B[j + 16 + LD * p] = fma(c, ap1, -sn * aq1);
+        B[j + LD * q] = fma(sn, ap0, c * aq0);
+        B[j + 16 + LD * q] = fma(sn, ap1, c * aq1);
+      }
+      if (rnd < ne - 2) __syncthreads();
     }
-    const int any = rot_any;
-    __syncthreads();
-    if (tid == 0) rot_any = 0;
-    __syncthreads();
+    // quadratic convergence: once every pair of a sweep met |cos| <= 1e-8 the
+    // rotated pairs are left at <= 1e-15 and the rest moved by second-order
+    // terms only -- no verification sweep
+    const int any = __syncthreads_or(big);
 #ifdef TR_RITZ_PROBE
     ++nsweeps;
 #endif

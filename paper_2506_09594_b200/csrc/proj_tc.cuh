@@ -7,12 +7,18 @@
 //   warp 0     TMA producer: A tile = 128 columns of the unfolding x 32 rows
 //              (K), K-major 128B-swizzled by the tensor map, plus the matching
 //              32-row chunks of Z_hi / Z_lo, into a kPwStages-deep ring;
-//   warps 2-5  split A_lo = A - tf32(A) next to each landed tile (3xTF32:
-//              A Z_hi + A Z_lo + A_lo Z_hi, fp32-faithful);
-//   warp 1     one thread issues tcgen05.mma.cta_group::1.kind::tf32
-//              (M=128 N=32 K=8) into a double-buffered TMEM accumulator and
-//              frees ring slots with tcgen05.commit;
-//   warps 6-9  epilogue: tcgen05.ld of a finished tile -> W rows in HBM and
+//   warps 2-9  split A_lo = A - tf32(A) of each landed tile straight into
+//              TENSOR MEMORY (tcgen05.st: lane = tile row, 32 columns = the 32
+//              K values) -- 3xTF32: A Z_hi + A Z_lo + A_lo Z_hi, fp32-faithful.
+//              A_lo never round-trips through shared memory (the smem-resident
+//              version moved 6.25 smem bytes per streamed byte, over the
+//              128 B/clk port at the HBM rate; this one 4.25);
+//   warp 1     one thread issues tcgen05.mma.cta_group::1.kind::tf32:
+//              A[smem] x [Z_hi | Z_lo] (M=128 N=64 K=8) as soon as the TMA tile
+//              lands, then A_lo[tmem] x Z_hi (N=32) once the split is in TMEM,
+//              into a double-buffered TMEM accumulator; frees ring slots with
+//              tcgen05.commit;
+//   warps 10-13 epilogue: tcgen05.ld of a finished tile -> W rows in HBM and
 //              the tile's 32 x 32 Gram W^T W accumulated in fp64 (the per-CTA
 //              partial of M), while the next tile accumulates in the other
 //              TMEM buffer.
@@ -46,6 +52,16 @@ __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t da, uint64_t
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+
+// same with the A operand in tensor memory (lane = M row, one K value per column)
+__device__ __forceinline__ void umma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(accumulate));
 }
 
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
@@ -82,6 +98,21 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 32 consecutive 32-bit TMEM columns of this thread's lane <- v
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]),
+      "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]),
+      "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]),
+      "r"(r[30]), "r"(r[31])
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
 // Z (m x 32, column-major, zero beyond s) split into tf32 high / low parts
 __global__ void k_split_z(const double* __restrict__ Z, int64_t m, int s,
                           float* __restrict__ zhi, float* __restrict__ zlo) {
@@ -95,11 +126,14 @@ __global__ void k_split_z(const double* __restrict__ Z, int64_t m, int s,
   zlo[e] = (float)(z - (double)hi);
 }
 
-constexpr int kPwStages = 6;   // TMA ring: A, Z_hi, Z_lo
-constexpr int kPwLo = 4;       // A_lo ring (split warps -> MMA)
-constexpr int kPwThreads = 320;
+constexpr int kPwStages = 8;   // TMA ring: A, Z_hi, Z_lo
+constexpr int kPwLo = 8;       // A_lo ring in tensor memory (split warps -> MMA): 32 columns each
+constexpr int kPwThreads = 448;
 constexpr int kPwStageBytes = kPjTileBytes + 2 * kPjZBytes;
-constexpr int kPwSmemBytes = kPwStages * kPwStageBytes + kPwLo * kPjTileBytes;
+constexpr int kPwSmemBytes = kPwStages * kPwStageBytes;
+constexpr int kPwTmemCols = 512;   // 2 accumulators x 64 + 2 lo accumulators x 32 + kPwLo x 32
+constexpr int kPwTmemAccLo = 128;  // accumulators of A_lo Z_hi
+constexpr int kPwTmemLo = 192;     // first A_lo column
 
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
                                             uint64_t* bar) {
@@ -135,8 +169,8 @@ __global__ void __launch_bounds__(kPwThreads, 1)
   const int64_t iters = my_tiles * kt;
 
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
-        smem_u32(&tmem_base_s)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+        smem_u32(&tmem_base_s)), "n"(kPwTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (threadIdx.x == 0) {
@@ -190,53 +224,61 @@ __global__ void __launch_bounds__(kPwThreads, 1)
           const int64_t it = t * kt + kk;
           const int st = (int)(it % kPwStages);
           const int ls = (int)(it % kPwLo);
-          mbar_wait(&lo_ready[ls], (uint32_t)((it / kPwLo) & 1));
-          tc_fence_after();
           const uint32_t sa = sbase + (uint32_t)(st * kPwStageBytes);
           const uint64_t dA = umma_desc_sw128(sa);
-          const uint64_t dAl =
-              umma_desc_sw128(sbase + (uint32_t)(kPwStages * kPwStageBytes + ls * kPjTileBytes));
           const uint64_t dZh = umma_desc_sw128(sa + kPjTileBytes);
+          mbar_wait(&full[st], (uint32_t)((it / kPwStages) & 1));
+          tc_fence_after();
 #pragma unroll
           for (int k = 0; k < 4; ++k) {  // K = 8 per MMA: +32 B in the swizzled row
             const uint64_t adv = (uint64_t)(2 * k);
             umma_tf32(d, dA + adv, dZh + adv, idesc64, (kk == 0 && k == 0) ? 0u : 1u);
-            umma_tf32(d, dAl + adv, dZh + adv, idesc, 1u);
           }
+          mbar_wait(&lo_ready[ls], (uint32_t)((it / kPwLo) & 1));
+          tc_fence_after();
+          const uint32_t ta = tmem + (uint32_t)(kPwTmemLo + 32 * ls);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)  // K = 8 per MMA: 8 TMEM columns of A_lo
+            umma_tf32_ts(tmem + (uint32_t)(kPwTmemAccLo + 32 * acc), ta + (uint32_t)(8 * k),
+                         dZh + (uint64_t)(2 * k), idesc, (kk == 0 && k == 0) ? 0u : 1u);
           umma_commit(&empty[st]);
           umma_commit(&lo_empty[ls]);
         }
         umma_commit(&tfull[acc]);
       }
     }
-  } else if (warp < 6) {  // ---- A_lo split ----
-    const int ct = threadIdx.x - 64;
-    for (int64_t it = 0; it < iters; ++it) {
+  } else if (warp < 10) {  // ---- A_lo split into tensor memory ----
+    // this warp may touch TMEM lanes 32 (warp % 4) ..: thread = tile row (M index).
+    // Two warps per lane quarter take alternate K-steps: the chain of one step
+    // (wait, 8 LDS.128, split, tcgen05.st + wait::st, arrive) is longer than
+    // the step's share of the HBM stream.
+    const int row = 32 * (warp & 3) + lane;
+    for (int64_t it = (warp - 2) >> 2; it < iters; it += 2) {
       const int st = (int)(it % kPwStages);
       const int ls = (int)(it % kPwLo);
       mbar_wait(&lo_empty[ls], (uint32_t)(((it / kPwLo) & 1) ^ 1));
       mbar_wait(&full[st], (uint32_t)((it / kPwStages) & 1));
-      const unsigned char* sp = smem + st * kPwStageBytes;
-      unsigned char* lp = smem + kPwStages * kPwStageBytes + ls * kPjTileBytes;
+      tc_fence_after();
+      // row `row` of the 128B-swizzled tile: 16-byte chunk c sits at c ^ (row & 7)
+      const unsigned char* sp = smem + st * kPwStageBytes + row * 128;
+      uint32_t lo[32];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const uint32_t off = (uint32_t)(ct + 128 * u) * 16u;  // swizzle-agnostic: same offset
-        const float4 a = *reinterpret_cast<const float4*>(sp + off);
-        float4 lo;
-        lo.x = a.x - __uint_as_float(__float_as_uint(a.x) & 0xFFFFE000u);
-        lo.y = a.y - __uint_as_float(__float_as_uint(a.y) & 0xFFFFE000u);
-        lo.z = a.z - __uint_as_float(__float_as_uint(a.z) & 0xFFFFE000u);
-        lo.w = a.w - __uint_as_float(__float_as_uint(a.w) & 0xFFFFE000u);
-        *reinterpret_cast<float4*>(lp + off) = lo;
+      for (int c = 0; c < 8; ++c) {
+        const float4 a = *reinterpret_cast<const float4*>(sp + ((c ^ (row & 7)) << 4));
+        lo[4 * c + 0] = __float_as_uint(a.x - __uint_as_float(__float_as_uint(a.x) & 0xFFFFE000u));
+        lo[4 * c + 1] = __float_as_uint(a.y - __uint_as_float(__float_as_uint(a.y) & 0xFFFFE000u));
+        lo[4 * c + 2] = __float_as_uint(a.z - __uint_as_float(__float_as_uint(a.z) & 0xFFFFE000u));
+        lo[4 * c + 3] = __float_as_uint(a.w - __uint_as_float(__float_as_uint(a.w) & 0xFFFFE000u));
       }
-      fence_async_smem();
+      tmem_st32(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(kPwTmemLo + 32 * ls), lo);
+      tc_fence_before();
       mbar_arrive(&lo_ready[ls]);
     }
   } else {  // ---- epilogue: TMEM lane quarter (warp % 4) ----
     __shared__ float wt[128][33];
     const int q = warp & 3;
     const int row = 32 * q + lane;
-    const int et = threadIdx.x - 192;  // 0..127: Gram entries et + 128 u
+    const int et = threadIdx.x - 320;  // 0..127: Gram entries et + 128 u
     double g[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) g[u] = 0.0;
@@ -248,7 +290,10 @@ __global__ void __launch_bounds__(kPwThreads, 1)
       tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * 64), w);
       tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * 64 + 32), wl);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) w[j] += wl[j];  // A Z_hi + A_lo Z_hi + A Z_lo
+      for (int j = 0; j < 32; ++j) w[j] += wl[j];  // A Z_hi + A Z_lo
+      tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(kPwTmemAccLo + 32 * acc), wl);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) w[j] += wl[j];  // + A_lo Z_hi
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
       const int64_t col = (blockIdx.x + t * gridDim.x) * 128 + row;
@@ -281,7 +326,7 @@ __global__ void __launch_bounds__(kPwThreads, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kPwTmemCols));
   }
 }
 
