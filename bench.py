@@ -434,28 +434,11 @@ def run_ours(args):
     algo = {k: v * lrta_per_step for k, v in lrta_bytes(dims, 4).items()}
     if args.step == "admm":
         algo.update(admm_bytes(dims, 4, len(WORKLOAD["modes"])))
-    cats = {k: v for k, v in prof.items() if k in algo}
-    dom = max(cats, key=lambda k: cats[k][0]) if cats else None
-    roof = None
-    if dom:
-        tot_ms, n_launch = cats[dom]
-        per_step_ms = tot_ms / prof_steps
-        achieved = algo[dom] / (per_step_ms / 1e3) / 1e9
-        tcat, tsrc = measured_traffic()
-        traffic = tcat.get(dom, {}).get("bytes_per_step")
-        roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
-                "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                "traffic": traffic, "traffic_unit": "DRAM bytes per step (ncu, summed over launches)",
-                "traffic_source": tsrc, "share_of_step": round(per_step_ms / ms_per_step, 4),
-                "algorithmic_bytes_per_step": algo[dom],
-                "launches_per_step": n_launch / prof_steps,
-                "note": "kernel time from CUDA events in a separate untimed pass of the same "
-                        "sweeps; event times of the 3 concurrent mode streams overlap; "
-                        "uncontended per-kernel times are in profiles/"}
     # The north_star's named target, the batched Krylov products, measured on
     # their own: a standalone t-SVT of the same resident tensor (one stream,
     # nothing concurrent), panel passes timed by events on their stream.
     roof_k = None
+    prof_k, reps_k = None, 1
     if rank == 0 and not sharded:
         out_k = ColMajor(torch.empty_like(flat), dims, "torch", None)
         tau_k = 0.05 * float(flat.norm()) / math.sqrt(N)
@@ -466,7 +449,7 @@ def run_ours(args):
         tsvt()
         torch.cuda.synchronize()
         lib.tr_profile_enable(1)
-        reps = 3
+        reps = reps_k = 3
         for _ in range(reps):
             tsvt()
         torch.cuda.synchronize()
@@ -485,6 +468,39 @@ def run_ours(args):
         roof_k["how"] = ("standalone randomized t-SVT of the bench tensor (no concurrent streams); "
                          "includes the small mode-1 passes")
         del out_k
+    # Dominant kernel category by UNCONTENDED device time per step.  The per-mode
+    # t-SVT chains of an ADMM sweep run on concurrent streams, so the event times
+    # of their kernels overlap one another (a pass that queues behind another
+    # mode's pass is charged the wait); for those categories the time comes from
+    # the standalone t-SVT above (x t-SVTs per step).  The main-stream kernels of
+    # the sweep (FFT solve, t-SVT inputs, fused tail) run with nothing beside them.
+    cats = {k: v[0] / prof_steps for k, v in prof.items() if k in algo}
+    src = {k: "sweep pass (main stream, nothing concurrent)" for k in cats}
+    nl = {k: prof[k][1] / prof_steps for k in cats}
+    if args.step == "admm" and prof_k is not None:
+        for k in cats:
+            if k in prof_k:
+                cats[k] = prof_k[k][0] / reps_k * lrta_per_step
+                nl[k] = prof_k[k][1] / reps_k * lrta_per_step
+                src[k] = "standalone t-SVT pass (one stream) x t-SVTs per step"
+    dom = max(cats, key=lambda k: cats[k]) if cats else None
+    roof = None
+    if dom:
+        per_step_ms = cats[dom]
+        achieved = algo[dom] / (per_step_ms / 1e3) / 1e9
+        tcat, tsrc = measured_traffic()
+        traffic = tcat.get(dom, {}).get("bytes_per_step")
+        roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                "traffic": traffic, "traffic_unit": "DRAM bytes per step (ncu, summed over launches)",
+                "traffic_source": tsrc, "share_of_step": round(per_step_ms / ms_per_step, 4),
+                "algorithmic_bytes_per_step": algo[dom],
+                "launches_per_step": nl[dom], "kernel_ms_per_step": round(per_step_ms, 4),
+                "timed_in": src[dom],
+                "note": "kernel time from CUDA events on the kernel's own stream in a separate "
+                        "untimed pass; the dominant category is chosen by uncontended time "
+                        "(kernel_ms_per_step below holds the raw event times of the concurrent "
+                        "sweep, where the three mode streams overlap)"}
     extra = {}
     if rank == 0 and args.step == "admm" and not args.no_legs:
         extra["fp64"] = fp64_leg(torch, pk, NativeSolver, ColMajor, lib, flat, dims, mask_dev,

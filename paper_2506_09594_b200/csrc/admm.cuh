@@ -78,6 +78,7 @@ struct Solver {
   int64_t ws_bytes = 0;
   std::vector<cudaStream_t> streams;
   std::vector<cudaEvent_t> evs;
+  std::vector<cudaEvent_t> evs_mid;  // per mode: the passes over the whole tensor are done
   cudaEvent_t ev_main = nullptr;
   SolveSpec ss;
   bool generic = false;  // low-rank step through the generic Tucker engine (tucker.cuh)
@@ -118,6 +119,7 @@ struct Solver {
     if (hres_max) cudaFreeHost(hres_max);
     for (auto s : streams) cudaStreamDestroy(s);
     for (auto e : evs) cudaEventDestroy(e);
+    for (auto e : evs_mid) cudaEventDestroy(e);
     if (ev_main) cudaEventDestroy(ev_main);
   }
   bool onebit() const { return cfg.kind >= 2; }
@@ -618,7 +620,7 @@ static int generic_svt(Solver<T>& s, const T* X, T* out, double tau, cudaStream_
 }
 
 template <typename T, typename F>
-static int low_rank_step(Solver<T>& s, double tau, F&& on_main) {
+static int low_rank_step(Solver<T>& s, double tau, F&& on_main, bool main_after_mode0 = false) {
   // fork: each mode on its own stream after the main stream's LRTA inputs
   // (TR_SERIAL_MODES: all on the main stream, for uncontended kernel timings)
   static const bool serial = getenv("TR_SERIAL_MODES") != nullptr;
@@ -632,13 +634,18 @@ static int low_rank_step(Solver<T>& s, double tau, F&& on_main) {
     else if (s.cfg.randomized)
       rc = gnhtsvt_randomized_t<T>(s.X[k], s.gnew[k], s.sh, s.cfg.seed, s.cfg.tkind, s.cfg.tmats,
                                    s.cfg.talphas, s.cfg.phi, tau, nullptr, nullptr, s.ws[k],
-                                   s.ws_bytes, sk);
+                                   s.ws_bytes, sk, main_after_mode0 ? s.evs_mid[k] : nullptr);
     else
       rc = full_svt<T>(s, s.X[k], s.gnew[k], tau, s.ws[k], sk);
     if (rc) return rc;
     TR_CUDA(cudaEventRecord(s.evs[k], sk));
   }
-  on_main();  // work of the main stream that overlaps the per-mode chains
+  // work of the main stream that overlaps the per-mode chains; main_after_mode0:
+  // only their latency-bound second halves (core-sized data, HBM nearly idle)
+  if (main_after_mode0 && !serial && !s.generic && s.cfg.randomized)
+    for (int k = 0; k < s.cfg.nmodes; ++k)
+      TR_CUDA(cudaStreamWaitEvent(s.streams[0], s.evs_mid[k], 0));
+  on_main();
   for (int k = 0; k < s.cfg.nmodes; ++k) TR_CUDA(cudaStreamWaitEvent(s.streams[0], s.evs[k], 0));
   return 0;
 }
@@ -768,11 +775,14 @@ static int admm_step(Solver<T>& s, double* hout) {
     const double q0 = s.cfg.psi.p0, q1 = s.cfg.psi.p1;
     // E', Y' need only L: with TR_OVERLAP_NOISE they run on the main stream
     // while the per-mode t-SVTs run and the fused tail reads them instead of
-    // recomputing them.  Off by default: on the bench workload the extra
-    // streaming blocks delay the mode chains' latency kernels more than the
-    // shorter tail saves (9.62 vs 9.31 ms per sweep).
-    static const bool overlap_env = getenv("TR_OVERLAP_NOISE") != nullptr;
-    const bool overlap = fuse && overlap_env;
+    // recomputing them.  = 1: from the start of the t-SVTs (slower on the bench
+    // workload: the extra streaming blocks delay the mode chains' passes,
+    // 7.64 vs 7.17 ms per sweep); = 2: once every mode has finished its passes
+    // over the whole tensor, when the chains work on the small cores and HBM
+    // is nearly idle.
+    static const int overlap_env = getenv("TR_OVERLAP_NOISE") ? atoi(getenv("TR_OVERLAP_NOISE")) : 0;
+    const bool overlap = fuse && overlap_env > 0;
+    const bool overlap_late = overlap && overlap_env >= 2 && s.cfg.randomized && !s.generic;
     overlap_noise = overlap;
     auto group_scale = [&] {
       if (structure == 1 || structure == 2) {
@@ -785,8 +795,12 @@ static int admm_step(Solver<T>& s, double* hout) {
 #undef TR_GS
       }
     };
+    // overlapping the mode chains' latency kernels: leave them thread slots on every SM
+    static const int late_ctas = getenv("TR_NOISE_CTAS") ? atoi(getenv("TR_NOISE_CTAS")) : 3;
+    const unsigned ngrid =
+        overlap_late ? (unsigned)std::min<int64_t>(grid, (int64_t)late_ctas * num_sms()) : grid;
 #define TR_ND2(K, S)                                                                          \
-  launch("noise_dual", v4 ? k_noise_dual<T, K, S, 4> : k_noise_dual<T, K, S, 1>, grid,        \
+  launch("noise_dual", v4 ? k_noise_dual<T, K, S, 4> : k_noise_dual<T, K, S, 1>, ngrid,       \
          kRedThreads, 0, st, g, s.A, s.mask,                                                   \
          (const T*)s.l, (const T*)s.lold, s.e, s.y, mu, q0, q1, level, (const double*)s.scale, \
          part)
@@ -800,12 +814,12 @@ static int admm_step(Solver<T>& s, double* hout) {
     auto noise_dual = [&] {
       group_scale();
       TR_PEN_DISPATCH(s.cfg.psi.kind, TR_ND)
-      launch("final_reduce", k_final_reduce, 1, 256, 0, st, (const double*)part, (int)rb, 7,
+      launch("final_reduce", k_final_reduce, 1, 256, 0, st, (const double*)part, (int)ngrid, 7,
              0b0010101u, res + 64);
     };
     if (low_rank_step<T>(s, tau, [&] {
           if (overlap) noise_dual();
-        }))
+        }, overlap_late))
       return 2;
     if (s.sharded)  // D_last^T G_new in the next right-hand side
       for (int k = 0; k < nm; ++k)
@@ -1120,6 +1134,8 @@ static int admm_create(const AdmmConfig& cfg, int order, const int64_t* dims, co
       cudaEvent_t e;
       TR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       s->evs.push_back(e);
+      TR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      s->evs_mid.push_back(e);
     }
   }
   TR_CUDA(cudaEventCreateWithFlags(&s->ev_main, cudaEventDisableTiming));

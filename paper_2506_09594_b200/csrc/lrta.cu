@@ -558,7 +558,7 @@ static int bki_mode(const Shape& sh, const T* A, int64_t m, int64_t n, int r, in
 
 template <typename T>
 static int lrta_compress(const T* a, const Shape& sh, uint64_t seed, const T* g0, const T* g1,
-                         Bufs<T>& bf, cudaStream_t st) {
+                         Bufs<T>& bf, cudaStream_t st, cudaEvent_t after_mode0 = nullptr) {
   static bool attr = false;
   if (!attr) {
     TR_CUDA(cudaFuncSetAttribute(k_ritz<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -571,9 +571,21 @@ static int lrta_compress(const T* a, const Shape& sh, uint64_t seed, const T* g0
   if (bki_mode<T>(sh, a, sh.n1, nA0, (int)sh.r0, (int)sh.b0, (int)sh.q0, sk0, g0, bf, bf.V0,
                   bf.F0, bf.F0t, bf.info, st))
     return 2;
+  // the passes over the whole tensor are done: what follows streams the small
+  // core only (the caller may schedule HBM-bound work of another stream here)
+  if (after_mode0) TR_CUDA(cudaEventRecord(after_mode0, st));
   // core rows -> mode-1 unfolding (n2 x r0*nf), contiguous columns
-  launch("core_from_w", k_core_from_w<T, T>, (unsigned)cdiv(nA0, 256), 256, 0, st,
-      bf.W, nA0, (int)sh.s0, bf.V0, (int)sh.r0, sh.n2, bf.A1);
+  if constexpr (sizeof(T) == 4) {
+    if (sh.s0 <= 32 && sh.r0 <= 32)
+      launch("core_from_w", k_core_from_w_s<T>, (unsigned)cdiv(nA0, 256), 256, 0, st,
+             (const float*)bf.W, nA0, (int)sh.s0, (const double*)bf.V0, (int)sh.r0, sh.n2, bf.A1);
+    else
+      launch("core_from_w", k_core_from_w<T, T>, (unsigned)cdiv(nA0, 256), 256, 0, st,
+             bf.W, nA0, (int)sh.s0, bf.V0, (int)sh.r0, sh.n2, bf.A1);
+  } else {
+    launch("core_from_w", k_core_from_w<T, T>, (unsigned)cdiv(nA0, 256), 256, 0, st,
+           bf.W, nA0, (int)sh.s0, bf.V0, (int)sh.r0, sh.n2, bf.A1);
+  }
   // mode 1 on the core (m = n2, n = r0 * nf); logical columns use r0_eff
   SketchSpec sk1{seed, 1, sh.r0, bf.info + 1, sh.r0 * sh.f0};
   if (bki_mode<T>(sh, bf.A1, sh.n2, nA1, (int)sh.r1, (int)sh.b1, (int)sh.q1, sk1, g1, bf, bf.V1,
@@ -797,13 +809,15 @@ template <typename T>
 static int gnhtsvt_randomized_t(const void* a, void* out, const Shape& sh, uint64_t seed,
                                 int kind, const void* mats, const double* alphas, Penalty pen,
                                 double tau, const void* g0, const void* g1, void* ws,
-                                int64_t ws_bytes, cudaStream_t st) {
+                                int64_t ws_bytes, cudaStream_t st,
+                                cudaEvent_t after_mode0 = nullptr) {
   Carve cv(ws);
   Bufs<T> bf;
   carve<T>(cv, sh, bf);
   TR_REQUIRE(ws_bytes >= cv.off, "workspace too small: %lld < %lld", (long long)ws_bytes,
              (long long)cv.off);
-  if (lrta_compress<T>((const T*)a, sh, seed, (const T*)g0, (const T*)g1, bf, st)) return 2;
+  if (lrta_compress<T>((const T*)a, sh, seed, (const T*)g0, (const T*)g1, bf, st, after_mode0))
+    return 2;
   if (core_svt<T>(sh, kind, (const cplx*)mats, alphas, pen, tau, bf, st)) return 2;
   return expand<T>(sh, bf, (T*)out, st);
 }

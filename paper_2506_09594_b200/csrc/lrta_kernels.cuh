@@ -1129,6 +1129,42 @@ __global__ void __launch_bounds__(256) k_ritz_apply(const double* __restrict__ Z
   if (tid == 0) *ticket = 0u;
 }
 
+// The same for fp32 W rows of s <= 32 values with the CTA's 256 rows staged
+// through shared memory by coalesced loads (row stride s | 1: conflict-free
+// reads): a thread reading its own row straight from global memory touches
+// s cache lines per load instruction (48 us for the 131072 x 28 W of the bench
+// t-SVT, against ~10 us here).
+template <typename TO>
+__global__ void __launch_bounds__(256) k_core_from_w_s(const float* __restrict__ W, int64_t n, int s,
+                                                       const double* __restrict__ V, int r,
+                                                       int64_t inner, TO* __restrict__ out) {
+  __shared__ double vs[32 * 32];
+  __shared__ float ws[256 * 33];
+  const int tid = threadIdx.x, ld = s | 1;
+  for (int e = tid; e < s * r; e += 256) vs[e] = V[e];
+  const int64_t c0 = (int64_t)blockIdx.x * 256;
+  const int cols = (int)(n - c0 < 256 ? n - c0 : 256);
+  const float* src = W + c0 * s;
+  for (int e = tid; e < cols * s; e += 256) {
+    const int row = e / s, j = e - row * s;
+    ws[row * ld + j] = src[e];
+  }
+  __syncthreads();
+  if (tid >= cols) return;
+  const int64_t c = c0 + tid;
+  const int64_t lo = c % inner, f = c / inner;
+  double w[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) w[j] = j < s ? (double)ws[tid * ld + j] : 0.0;
+  for (int i = 0; i < r; ++i) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < s) acc += w[j] * vs[j + s * i];
+    out[lo + inner * (i + (int64_t)r * f)] = (TO)acc;
+  }
+}
+
 // core rows from W: out[lo + inner*(i + r*f)] = sum_j W[c*s + j] V[j + s*i],
 // c = lo + inner * f.  Realises F^T A (sketch.py:267-269) without another pass.
 // One thread per unfolding column c: its W row (s values) times V (s x r,
