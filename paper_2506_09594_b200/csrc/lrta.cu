@@ -301,9 +301,9 @@ static int64_t panel_mma(const float* A, int64_t m, int64_t n, int b, const floa
     pa.nst = 2;
     pa.nchunks = cdiv(n, kPmCols);
     if (MODE == 0) {
-      const int64_t total = pa.nchunks * kPmCols * bw;
+      const int64_t total = pa.nchunks * kPmCols;  // one thread per (padded) column
       launch("sketch_rows", k_sketch_rows,
-             (unsigned)std::min<int64_t>(cdiv(total, 256), 4 * num_sms()), 256, 0, st, n, bw, sk,
+             (unsigned)std::min<int64_t>(cdiv(total, 128), 8 * num_sms()), 128, 0, st, n, bw, sk,
              gover, rows, j0, b);
     }
     const float* cf = MODE == 0 ? rows : nullptr;
