@@ -79,6 +79,7 @@ struct Solver {
   std::vector<cudaStream_t> streams;
   std::vector<cudaEvent_t> evs;
   std::vector<cudaEvent_t> evs_mid;  // per mode: the passes over the whole tensor are done
+  std::vector<char> tf_built;        // per mode: transform matrices live in its workspace
   cudaEvent_t ev_main = nullptr;
   SolveSpec ss;
   bool generic = false;  // low-rank step through the generic Tucker engine (tucker.cuh)
@@ -634,10 +635,15 @@ static int low_rank_step(Solver<T>& s, double tau, F&& on_main, bool main_after_
     else if (s.cfg.randomized)
       rc = gnhtsvt_randomized_t<T>(s.X[k], s.gnew[k], s.sh, s.cfg.seed, s.cfg.tkind, s.cfg.tmats,
                                    s.cfg.talphas, s.cfg.phi, tau, nullptr, nullptr, s.ws[k],
-                                   s.ws_bytes, sk, main_after_mode0 ? s.evs_mid[k] : nullptr);
+                                   s.ws_bytes, sk, main_after_mode0 ? s.evs_mid[k] : nullptr,
+                                   !s.tf_built.empty() && s.tf_built[k]);
     else
       rc = full_svt<T>(s, s.X[k], s.gnew[k], tau, s.ws[k], sk);
     if (rc) return rc;
+    if (!s.generic && s.cfg.randomized) {
+      if (s.tf_built.empty()) s.tf_built.assign(s.cfg.nmodes, 0);
+      s.tf_built[k] = 1;  // same shape, kind and workspace on every later sweep
+    }
     TR_CUDA(cudaEventRecord(s.evs[k], sk));
   }
   // work of the main stream that overlaps the per-mode chains; main_after_mode0:

@@ -234,17 +234,24 @@ __device__ __forceinline__ void block_partials(double (&v)[NQ], unsigned is_max,
   }
 }
 
+// One warp per quantity (fixed order: lane-strided partials, then the xor tree):
+// the quantities reduce side by side instead of one block-wide reduction each.
 __global__ void k_final_reduce(const double* __restrict__ part, int nblocks, int nq,
                                unsigned is_max, double* __restrict__ out) {
-  __shared__ double red[32];
-  for (int q = 0; q < nq; ++q) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int q = warp; q < nq; q += nw) {
+    const bool mx = (is_max >> q) & 1;
     double v = 0.0;
-    for (int b = threadIdx.x; b < nblocks; b += blockDim.x) {
+    for (int b = lane; b < nblocks; b += 32) {
       const double x = part[(int64_t)b * nq + q];
-      v = (is_max >> q) & 1 ? fmax(v, x) : v + x;
+      v = mx ? fmax(v, x) : v + x;
     }
-    v = (is_max >> q) & 1 ? block_max(v, red) : block_sum(v, red);
-    if (threadIdx.x == 0) out[q] = v;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double x = __shfl_xor_sync(0xffffffffu, v, o);
+      v = mx ? fmax(v, x) : v + x;
+    }
+    if (lane == 0) out[q] = v;
   }
 }
 

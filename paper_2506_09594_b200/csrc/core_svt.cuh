@@ -356,6 +356,12 @@ __global__ void __launch_bounds__(16 * LPP) k_face_svt8(cplx* __restrict__ faces
   __shared__ double wsc[32];
   __shared__ double fred[32];
   cplx* src = faces + (int64_t)blockIdx.x * r0 * r1;
+  // the conjugate-mirror partner of this canonical face (k_mirror_fix fused here)
+  cplx* mir = nullptr;
+  if (mirror_tr.nt > 0) {
+    const int64_t mf = mirror_face(blockIdx.x, mirror_tr);
+    if (mf != (int64_t)blockIdx.x) mir = faces + mf * r0 * r1;
+  }
   const int tid = threadIdx.x;
   const int ne = r1 + (r1 & 1), npairs = ne / 2;
   for (int e = tid; e < (ne - 1) * npairs; e += NT) {
@@ -373,7 +379,11 @@ __global__ void __launch_bounds__(16 * LPP) k_face_svt8(cplx* __restrict__ faces
   }
   const double fn2 = block_sum(f2, fred);
   // zero face: prox(0) = 0, the face stays zero (non-finite input is left as is)
-  if (!(fn2 > 0.0) || !(fn2 < 1e300)) return;
+  if (!(fn2 > 0.0) || !(fn2 < 1e300)) {
+    if (mir)
+      for (int e = tid; e < r0 * r1; e += NT) mir[e] = cconj(X[e]);
+    return;
+  }
   int ex;
   frexp(sqrt(fn2), &ex);
   const double scale = ldexp(1.0, -ex), unscale = ldexp(1.0, ex);
@@ -531,7 +541,9 @@ __global__ void __launch_bounds__(16 * LPP) k_face_svt8(cplx* __restrict__ faces
       ar += a.re * b.re - a.im * b.im;
       ai += a.re * b.im + a.im * b.re;
     }
-    src[e] = {ar * unscale, ai * unscale};
+    const cplx o = {ar * unscale, ai * unscale};
+    src[e] = o;
+    if (mir) mir[e] = cconj(o);
   }
 }
 

@@ -373,7 +373,9 @@ static TsqrPlan tsqr_plan(int64_t m, int s, bool wide = false) {
 }
 
 template <typename T>
-static void orth_basis(int64_t m, int s, Bufs<T>& bf, int64_t* info, cudaStream_t st) {
+// Returns true when the kernel also wrote the tf32 split of Z (bf.zhi / bf.zlo)
+// that the tensor-core projection reads (fp32 unfoldings, cluster TSQR).
+static bool orth_basis(int64_t m, int s, Bufs<T>& bf, int64_t* info, cudaStream_t st) {
   static const bool cluster_off = getenv("TR_NO_ORTH_CLUSTER") != nullptr;
   if (!cluster_off && m <= (int64_t)kOcCtas * kOcRows && s <= kOcS) {
     static bool attr = false;
@@ -382,15 +384,16 @@ static void orth_basis(int64_t m, int s, Bufs<T>& bf, int64_t* info, cudaStream_
                            (int)kOcSmem);
       attr = true;
     }
+    const bool split = sizeof(T) == 4 && getenv("TR_NO_FUSED_ZSPLIT") == nullptr;
     launch("orth", k_orth_cluster<T>, kOcCtas, kOcThreads, kOcSmem, st, (const double*)bf.K, m, s,
-           bf.Z, bf.Zt, info);
-    return;
+           bf.Z, bf.Zt, info, split ? bf.zhi : (float*)nullptr, split ? bf.zlo : (float*)nullptr);
+    return split;
   }
   TsqrPlan p = tsqr_plan(m, s);
   if (!p.ok) p = tsqr_plan(m, s, true);
   if (!p.ok) {
     launch("orth", k_orth<T>, 1, 1024, 0, st, bf.K, m, s, bf.work, bf.Z, bf.Zt, info);
-    return;
+    return false;
   }
   static bool attr = false;
   if (!attr) {
@@ -407,6 +410,7 @@ static void orth_basis(int64_t m, int s, Bufs<T>& bf, int64_t* info, cudaStream_
          0.0, 1, (double*)nullptr);
   launch("orth", k_tsqr_form<T>, p.nb, tq_threads, p.sm_form, st, bf.work, bf.tq_tau, bf.tq_C,
          (int)nrows, m, s, p.RB, bf.Z, bf.Zt);
+  return false;
 }
 
 // W = A^T Z and M = W^T W on the tensor cores (proj_tc.cuh) for fp32
@@ -450,7 +454,8 @@ static bool tmap_f32(CUtensorMap* map, const float* base, int64_t rows, int64_t 
 // W = A^T Z on the tensor cores (proj_tc.cuh) when the unfolding suits it:
 // s <= 32 in one pass with the fused Gram; 32 < s <= 64 as two column blocks
 // of W (two passes over A) and the Gram from W afterwards.
-static bool project(const float* A, int64_t m, int64_t n, int s, Bufs<float>& bf, cudaStream_t st) {
+static bool project(const float* A, int64_t m, int64_t n, int s, Bufs<float>& bf, cudaStream_t st,
+                    bool z_split_done = false) {
   if (m % 32 != 0 || s > 64 || ((uintptr_t)A % 16) != 0 || n >= (1ll << 31) ||
       getenv("TR_NO_TC") != nullptr)
     return false;
@@ -468,8 +473,9 @@ static bool project(const float* A, int64_t m, int64_t n, int s, Bufs<float>& bf
   }
   for (int j0 = 0; j0 < s; j0 += 32) {
     const int cnt = std::min(32, s - j0);
-    launch("proj_split", k_split_z, (unsigned)cdiv(m * 32, 256), 256, 0, st,
-           (const double*)(bf.Z + m * (int64_t)j0), m, cnt, bf.zhi, bf.zlo);
+    if (!(z_split_done && s <= 32))
+      launch("proj_split", k_split_z, (unsigned)cdiv(m * 32, 256), 256, 0, st,
+             (const double*)(bf.Z + m * (int64_t)j0), m, cnt, bf.zhi, bf.zlo);
     launch("proj_tc", k_proj_ws, (unsigned)grid, kPwThreads, smem, st, ma, mh, ml, m, n, cnt,
            bf.W + j0, s <= 32 ? bf.Mpart : (double*)nullptr, s);
   }
@@ -486,7 +492,7 @@ static bool project(const float* A, int64_t m, int64_t n, int s, Bufs<float>& bf
   return true;
 }
 
-static bool project(const double*, int64_t, int64_t, int, Bufs<double>&, cudaStream_t) {
+static bool project(const double*, int64_t, int64_t, int, Bufs<double>&, cudaStream_t, bool = false) {
   return false;
 }
 
@@ -527,8 +533,8 @@ static int bki_mode(const Shape& sh, const T* A, int64_t m, int64_t n, int r, in
     double* slot = bf.K + m * (int64_t)b * k;
     if (reduce_normalize(np, slot)) return 1;
   }
-  orth_basis<T>(m, s, bf, info, st);
-  if (!project(A, m, n, s, bf, st)) {
+  const bool z_split = orth_basis<T>(m, s, bf, info, st);
+  if (!project(A, m, n, s, bf, st, z_split)) {
     dot_cols<T>(A, m, n, bf.Zt, s, bf.W, st);
     const int64_t mparts = std::min<int64_t>(cdiv(n, 64), bf.max_mparts);
     const int64_t rpb = cdiv(n, mparts);
@@ -631,7 +637,8 @@ static void mode_product(const void* in, int in_real, void* out, int out_real, i
 // Transform-domain SVT of the r0 x r1 x trailing core in place (bf.core).
 template <typename T>
 static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* alphas,
-                    Penalty pen, double tau, Bufs<T>& bf, cudaStream_t st) {
+                    Penalty pen, double tau, Bufs<T>& bf, cudaStream_t st,
+                    bool transform_built = false) {
   const int64_t face = sh.r0 * sh.r1;
   const int nt = sh.tr.nt;
   const cplx* U[8];
@@ -643,7 +650,10 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
       U[i] = mats + uoff;
       al[i] = alphas[i];
     } else {
-      launch("build_transform", k_build_transform, (unsigned)cdiv((int64_t)n * n, 256), 256, 0, st, kind, n, bf.U + uoff);
+      // (a caller that owns the workspace across calls -- the ADMM solver -- keeps the matrices)
+      if (!transform_built)
+        launch("build_transform", k_build_transform, (unsigned)cdiv((int64_t)n * n, 256), 256, 0,
+               st, kind, n, bf.U + uoff);
       U[i] = bf.U + uoff;
       al[i] = kind == TR_TRANSFORM_FFT ? (double)n : 1.0;
     }
@@ -683,6 +693,7 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
                                  2 * 64 * 64 * (int)sizeof(cplx)));
     attr = true;
   }
+  bool mirror_done = false;
   if (sh.r0 > 64 || sh.r1 > 64) {
     // large faces (deterministic t-SVT of a whole tensor): X / V in global scratch,
     // X in the free mode-product buffer
@@ -699,6 +710,7 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
     }
     launch("face_svt", k_face_svt8<8>, (unsigned)nfa, 128, smem8, st, faces, (int)sh.r0,
            (int)sh.r1, pen, tau, mirror_tr);
+    mirror_done = true;  // the kernel writes the conjugate-mirror faces itself
   } else {
     // one warp per Jacobi pair: no idle warps at the per-round barrier
     static const int fth_env = getenv("TR_FACE_THREADS") ? atoi(getenv("TR_FACE_THREADS")) : 0;
@@ -707,7 +719,8 @@ static int core_svt(const Shape& sh, int kind, const cplx* mats, const double* a
     launch("face_svt", k_face_svt, (unsigned)nfa, fth, smem, st, faces, (int)sh.r0, (int)sh.r1,
            pen, tau, mirror_tr);
   }
-  if (kind == TR_TRANSFORM_FFT) launch("mirror_fix", k_mirror_fix, g, 256, 0, st, faces, face, nfa, sh.tr);
+  if (kind == TR_TRANSFORM_FFT && !(mirror_done && mirror_tr.nt > 0))
+    launch("mirror_fix", k_mirror_fix, g, 256, 0, st, faces, face, nfa, sh.tr);
   // inverse: U^H / alpha in reverse mode order, real part on the last step
   for (int i = nt - 1; i >= 0; --i) {
     const int n = (int)sh.tr.d[i];
@@ -810,7 +823,7 @@ static int gnhtsvt_randomized_t(const void* a, void* out, const Shape& sh, uint6
                                 int kind, const void* mats, const double* alphas, Penalty pen,
                                 double tau, const void* g0, const void* g1, void* ws,
                                 int64_t ws_bytes, cudaStream_t st,
-                                cudaEvent_t after_mode0 = nullptr) {
+                                cudaEvent_t after_mode0 = nullptr, bool transform_built = false) {
   Carve cv(ws);
   Bufs<T> bf;
   carve<T>(cv, sh, bf);
@@ -818,7 +831,7 @@ static int gnhtsvt_randomized_t(const void* a, void* out, const Shape& sh, uint6
              (long long)cv.off);
   if (lrta_compress<T>((const T*)a, sh, seed, (const T*)g0, (const T*)g1, bf, st, after_mode0))
     return 2;
-  if (core_svt<T>(sh, kind, (const cplx*)mats, alphas, pen, tau, bf, st)) return 2;
+  if (core_svt<T>(sh, kind, (const cplx*)mats, alphas, pen, tau, bf, st, transform_built)) return 2;
   return expand<T>(sh, bf, (T*)out, st);
 }
 

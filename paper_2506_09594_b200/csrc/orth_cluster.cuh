@@ -165,7 +165,8 @@ __device__ inline void col_apply_q(const double* V, int ldv, int nrows, int kmax
 template <typename T>
 __global__ void __cluster_dims__(kOcCtas, 1, 1) __launch_bounds__(kOcThreads, 1)
     k_orth_cluster(const double* __restrict__ K, int64_t m, int s, double* __restrict__ Z,
-                   T* __restrict__ Zt, int64_t* __restrict__ info) {
+                   T* __restrict__ Zt, int64_t* __restrict__ info, float* __restrict__ zhi,
+                   float* __restrict__ zlo) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) double oc_smem[];
@@ -376,19 +377,27 @@ __global__ void __cluster_dims__(kOcCtas, 1, 1) __launch_bounds__(kOcThreads, 1)
   }
   col_apply_q<kOcRpl>(vloc, kOcRows, rows_c, kloc, tau, zz, se);
   OC_MARK(6)
+  // zhi / zlo (optional): the tf32 high / low split of Z as an m x 32 block (zero
+  // columns beyond s_eff) for the tensor-core projection -- k_split_z fused here
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
-    const int j = warp + kOcWarps * q;
-    if (j < s)
+    const int j = warp + kOcWarps * q;  // < 32: the two passes cover every column of the split
 #pragma unroll
-      for (int r = 0; r < kOcRpl; ++r) {
-        const int row = lane + 32 * r;
-        if (row < rows_c) {
-          const double v = j < se ? zz[q][r] : 0.0;
+    for (int r = 0; r < kOcRpl; ++r) {
+      const int row = lane + 32 * r;
+      if (row < rows_c) {
+        const double v = (j < s && j < se) ? zz[q][r] : 0.0;
+        if (j < s) {
           Z[row0 + row + m * j] = v;
           Zt[row0 + row + m * j] = (T)v;
         }
+        if (zhi != nullptr) {
+          const float hi = __uint_as_float(__float_as_uint((float)v) & 0xFFFFE000u);
+          zhi[row0 + row + m * j] = hi;
+          zlo[row0 + row + m * j] = (float)(v - (double)hi);
+        }
       }
+    }
   }
   if (c == 0 && threadIdx.x == 0) info[0] = se;
   cl.sync();  // no CTA exits while a peer may still address its shared memory
