@@ -135,6 +135,34 @@ def test_zero_tensor_returns_zero(cuda_lib):
     assert np.all(out == 0)
 
 
+@pytest.mark.parametrize("scale", [1e20, 1e-20])
+def test_scale_invariance(cuda_lib, scale):
+    """The l1 t-SVT is positively homogeneous: the Jacobi rotations of the core
+    faces and of the Rayleigh-Ritz Gram (fp32 tangents on operands scaled by a
+    power of two) must not depend on the magnitude of the data."""
+    import paper_2506_09594_b200 as pk
+    x = _tensor((48, 40, 6), 0, 5)
+    ref = lrta.gnhtsvt_randomized(x, TransformSpec("fft"), PENS["l1"], 0.4, (9, 8), (3, 3), (2, 2),
+                                  (0, 1), philox.PhiloxSketchSource(4), canonical=True)
+    sk = pk.SketchConfig(ranks=(9, 8), blocks=(3, 3), krylov=(2, 2), seed=4)
+    got = pk.gnhtsvt_randomized(x * scale, pk.Transform.fft(), pk.L1(), 0.4 * scale, sk)
+    assert np.all(np.isfinite(got))
+    assert _rel(got / scale, ref) <= 1e-9
+
+
+def test_constant_along_the_transformed_mode(cuda_lib):
+    """Identical frontal slices: every transform-domain face but the first is
+    (numerically) zero -- tiny faces next to an O(1) one in the face SVT."""
+    import paper_2506_09594_b200 as pk
+    a = np.random.default_rng(9).standard_normal((40, 36))
+    x = np.repeat(a[:, :, None], 8, axis=2)
+    ref = lrta.gnhtsvt_randomized(x, TransformSpec("fft"), PENS["mcp"], 0.5, (8, 8), (3, 3), (2, 2),
+                                  (0, 1), philox.PhiloxSketchSource(6), canonical=True)
+    sk = pk.SketchConfig(ranks=(8, 8), blocks=(3, 3), krylov=(2, 2), seed=6)
+    got = pk.gnhtsvt_randomized(x, pk.Transform.fft(), pk.MCP(2.0), 0.5, sk)
+    assert _rel(got, ref) <= 1e-9
+
+
 def test_deflated_krylov_block(cuda_lib):
     """m < (q+1) b: the Krylov block deflates to rank m, as in the reference."""
     import paper_2506_09594_b200 as pk
