@@ -768,7 +768,11 @@ static bool expand_tc(const Shape& sh, Bufs<float>& bf, float* out, cudaStream_t
   launch("expand_split", k_split_rows, (unsigned)cdiv(sh.n1 * 32, 256), 256, 0, st,
          (const double*)bf.F0, sh.n1, (int)sh.r0, bf.f0h, bf.f0l);
   const int64_t nrb = sh.n1 / 128;
-  const int64_t per = std::max<int64_t>(1, std::min<int64_t>(stream_sms() / nrb, cdiv(N, 128)));
+  // SMs left to the latency kernels (face SVT, Ritz, TSQR) of the other mode
+  // chains while this HBM-write-bound pass runs (TR_EXPAND_RESERVE, default 0)
+  static const int ex_reserve = getenv("TR_EXPAND_RESERVE") ? atoi(getenv("TR_EXPAND_RESERVE")) : 0;
+  const int64_t per = std::max<int64_t>(
+      1, std::min<int64_t>(std::max(1, stream_sms() - ex_reserve) / nrb, cdiv(N, 128)));
   const size_t smem = (size_t)(direct ? kEtSmemBytes : kEtSmemBytesTs) + 1024;
   static bool attr = false;
   if (!attr) {

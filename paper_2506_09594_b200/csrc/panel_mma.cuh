@@ -86,6 +86,24 @@ __device__ __forceinline__ void split_trunc(float x, uint32_t& hi, uint32_t& lo)
   lo = __float_as_uint(x - __uint_as_float(hi));
 }
 
+// mbarrier wait / arrive on a precomputed shared-window address (the generic ->
+// shared conversion of a barrier pointer costs an S2UR + two address ops at
+// every use; the compute-warp loop does ~7 barrier operations per chunk)
+__device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t phase) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_a(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
 struct PanelMmaArgs {
   int64_t m, n;
   int b;
@@ -413,26 +431,36 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kPmThreads, 1)
         for (int i = 0; i < 4; ++i) y[rg][tl][i] = 0.f;
     const int rw0 = 32 * RG * warp;  // first row of this warp (rows >= m read zero padding)
 
-    // stage / phase of chunk `it` and of chunk it-2 (step 2 lags two chunks)
+    // stage / phase of chunk `it` and of chunk it-2 (step 2 lags two chunks).
+    // Everything the loop addresses is a precomputed shared-window offset, the
+    // counters are 32-bit (a CTA's chunk count is far below 2^31).
     int s_cur = 0, s_old = 0;
     uint32_t ph_cur = 0;
     const uint32_t zero2[2] = {0u, 0u};
-    for (int64_t it = 0; it < my_chunks + (MODE == 1 ? 2 : 0); ++it) {
-      const bool has1 = it < my_chunks;        // chunk it: step 1 (gram) / step 2 (sketch)
+    const uint32_t full_a = smem_u32(&full[0]), empty_a = smem_u32(&empty[0]);
+    const uint32_t redfull_a = smem_u32(&redfull[0]), redempty_a = smem_u32(&redempty[0]);
+    const uint32_t tready_a = smem_u32(&tready[0]), tempty_a = smem_u32(&tempty[0]);
+    const int nch = (int)my_chunks;
+    const int nit = nch + (MODE == 1 ? 2 : 0);
+    const int te0 = g * 8 + t;  // T[column t][sketch column g]
+    float* const rw_base = red + warp * kPmRS + g * 8 + 2 * t;
+    for (int it = 0; it < nit; ++it) {
+      const bool has1 = it < nch;              // chunk it: step 1 (gram) / step 2 (sketch)
       const bool has2 = MODE == 1 && it >= 2;  // chunk it-2: step 2 (gram)
-      const int kb = (int)(it & 1);
-      if (has1) mbar_wait(&full[s_cur], ph_cur);
+      const int kb = it & 1;
+      if (has1) mbar_wait_a(full_a + 8u * (uint32_t)s_cur, ph_cur);
       const float* As1 = stages + s_cur * stage_elems;
       uint32_t bh[2], bl[2];
       if (MODE == 1) {
         if (has2) {
-          mbar_wait(&tready[kb], (uint32_t)(((it - 2) >> 1) & 1));
-          const int e0 = g * 8 + t;  // T[column t][sketch column g]
-          bh[0] = __float_as_uint(thi[kb * kPmTE + e0]);
-          bh[1] = __float_as_uint(thi[kb * kPmTE + e0 + 4]);
-          bl[0] = __float_as_uint(tlo[kb * kPmTE + e0]);
-          bl[1] = __float_as_uint(tlo[kb * kPmTE + e0 + 4]);
-          mbar_arrive(&tempty[kb]);
+          mbar_wait_a(tready_a + 8u * (uint32_t)kb, (uint32_t)(((it - 2) >> 1) & 1));
+          const float* th = thi + kb * kPmTE + te0;
+          const float* tl = tlo + kb * kPmTE + te0;
+          bh[0] = __float_as_uint(th[0]);
+          bh[1] = __float_as_uint(th[4]);
+          bl[0] = __float_as_uint(tl[0]);
+          bl[1] = __float_as_uint(tl[4]);
+          mbar_arrive_a(tempty_a + 8u * (uint32_t)kb);
         }
         float d[4][4];
 #pragma unroll
@@ -444,22 +472,21 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kPmThreads, 1)
           panel_fused<RG, true, true>(As1, As2, S, rw0, g, t, pf, d, y, bh, bl);
         else if (has1)
           panel_fused<RG, true, false>(As1, As2, S, rw0, g, t, pf, d, y, zero2, zero2);
-        else
+        else if (has2)  // (neither: a one-chunk CTA between its step 1 and its step 2)
           panel_fused<RG, false, true>(As1, As2, S, rw0, g, t, pf, d, y, bh, bl);
         if (has2) {
-          mbar_arrive(&empty[s_old]);
+          mbar_arrive_a(empty_a + 8u * (uint32_t)s_old);
           s_old = s_old + 1 == nst ? 0 : s_old + 1;
         }
         if (has1) {
           // d[0..1] rows g (P_hi), d[2..3] rows g+8 (P_lo): T partial (sketch column g, columns 2t / 2t+1)
-          mbar_wait(&redempty[kb], (uint32_t)(((it >> 1) & 1) ^ 1));
-          float* rw = red + (kb * kPmWarps + warp) * kPmRS;
-          *reinterpret_cast<float2*>(rw + g * 8 + 2 * t) =
+          mbar_wait_a(redempty_a + 8u * (uint32_t)kb, (uint32_t)(((it >> 1) & 1) ^ 1));
+          *reinterpret_cast<float2*>(rw_base + kb * (kPmWarps * kPmRS)) =
               make_float2(((d[0][0] + d[1][0]) + (d[2][0] + d[3][0])) +
                               ((d[0][2] + d[1][2]) + (d[2][2] + d[3][2])),
                           ((d[0][1] + d[1][1]) + (d[2][1] + d[3][1])) +
                               ((d[0][3] + d[1][3]) + (d[2][3] + d[3][3])));
-          mbar_arrive(&redfull[kb]);
+          mbar_arrive_a(redfull_a + 8u * (uint32_t)kb);
         }
       } else {
         const float* cr = cst + s_cur * kPmCols * b;
@@ -469,7 +496,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kPmThreads, 1)
         split_tf32(v1, bh[1], bl[1]);
         float d[4][4];
         panel_fused<RG, false, true>(As1, As1, S, rw0, g, t, pf, d, y, bh, bl);
-        mbar_arrive(&empty[s_cur]);
+        mbar_arrive_a(empty_a + 8u * (uint32_t)s_cur);
       }
       if (has1) {
         s_cur = s_cur + 1 == nst ? 0 : s_cur + 1;
