@@ -190,6 +190,14 @@ int tr_admm_create(int dtype, int order, const int64_t* dims, int kind, const vo
                    uint64_t seed, int transform_kind, const void* transform_mats,
                    const double* alphas, void** handle);
 int tr_admm_step(void* handle, double* out);
+/* on != 0: tr_admm_step enqueues the L-solve and the t-SVT inputs of the NEXT
+ * sweep before it waits for this sweep's residuals, so the GPU does not idle
+ * across the host's read-back and stopping test (tenrec/solvers.py:270-272 tests
+ * on the host after every iteration).  The returned state (tr_admm_read) and
+ * every later residual are unchanged; a caller that stops after a step leaves
+ * that work unused -- switch it off before the last step of a fixed-length
+ * run.  Applies to the fused gradient chain on one GPU; ignored otherwise. */
+int tr_admm_lookahead(void* handle, int on);
 int tr_admm_read(void* handle, int which, void* dst, void* stream);
 int tr_admm_destroy(void* handle);
 /*

@@ -73,6 +73,7 @@ SIGNATURES = {
         _c_i64p, _c_i64p, _c_i64p, ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64,
         ctypes.POINTER(TrComm), ctypes.POINTER(ctypes.c_void_p)]),
     "tr_admm_step": (ctypes.c_int, [_vp, _c_dp]),
+    "tr_admm_lookahead": (ctypes.c_int, [_vp, ctypes.c_int]),
     "tr_admm_read": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp]),
     "tr_admm_destroy": (ctypes.c_int, [_vp]),
     "tr_admm_stream": (_vp, [_vp]),

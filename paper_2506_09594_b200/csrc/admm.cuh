@@ -69,6 +69,14 @@ struct Solver {
   std::vector<T*> gcur, gnew, lag, X;
   std::vector<T*> lag2;     // second multiplier buffer of the fused sweep tail
   bool rhs_ready = false;   // rhs already holds this sweep's L right-hand side
+  // Lookahead (tr_admm_lookahead): the L-solve and the t-SVT inputs of the next
+  // sweep are enqueued before the host waits for this sweep's residuals, so the
+  // GPU never idles across the host's read-back / stopping test.  They touch
+  // only buffers the returned state does not live in (the free L buffer, the
+  // spectrum, the t-SVT inputs); a solve that stops simply leaves them unused.
+  bool lookahead = false;
+  bool head_done = false;   // this sweep's L-solve and t-SVT inputs are already enqueued
+  cudaEvent_t ev_res = nullptr;
   cpx<T>* spec = nullptr;
   std::vector<cpx<T>*> tw;
   double* lam = nullptr;
@@ -122,6 +130,7 @@ struct Solver {
     for (auto e : evs) cudaEventDestroy(e);
     for (auto e : evs_mid) cudaEventDestroy(e);
     if (ev_main) cudaEventDestroy(ev_main);
+    if (ev_res) cudaEventDestroy(ev_res);
   }
   bool onebit() const { return cfg.kind >= 2; }
 };
@@ -763,7 +772,7 @@ static int admm_step(Solver<T>& s, double* hout) {
     // L-subproblem (solvers.py:231-233)
     if (pure) {
       launch("admm_rhs", rhs_k, grid, kRedThreads, 0, st, g, s.A, s.e, s.y, mu, gp, lp, s.l);
-    } else {
+    } else if (!s.head_done) {
       if (!s.rhs_ready)
         launch("admm_rhs", rhs_k, grid, kRedThreads, 0, st, g, s.A, s.e, s.y, mu, gp, lp, s.rhs);
       if (s.sharded) {
@@ -774,7 +783,8 @@ static int admm_step(Solver<T>& s, double* hout) {
       }
     }
     tau = 1.0 / (gamma * mu);
-    lrta_inputs<T>(s, s.l, mu, v4, grid, st);
+    if (!s.head_done) lrta_inputs<T>(s, s.l, mu, v4, grid, st);
+    s.head_done = false;
     // noise and dual updates (solvers.py:239-246)
     const double level = s.cfg.lam / mu;
     const int structure = s.cfg.kind == 1 ? 3 : s.cfg.structure;
@@ -919,7 +929,20 @@ static int admm_step(Solver<T>& s, double* hout) {
     TR_CUDA(cudaMemcpyAsync(s.hres_max, s.res_max, 128 * sizeof(double), cudaMemcpyDeviceToHost, st));
   }
   TR_CUDA(cudaMemcpyAsync(s.hres, res, 128 * sizeof(double), cudaMemcpyDeviceToHost, st));
-  TR_CUDA(cudaStreamSynchronize(st));
+  // lookahead: the next sweep's L-solve and t-SVT inputs go in behind the
+  // read-back (fused gradient chain on one GPU; the right-hand side is ready)
+  const bool ahead = s.lookahead && fuse && !s.sharded && !pure && s.rhs_ready;
+  if (ahead) {
+    TR_CUDA(cudaEventRecord(s.ev_res, st));
+    const double mu2 = std::min(s.cfg.mu_max, s.cfg.growth * s.mu);
+    // next sweep's buffers: L is solved into the buffer that holds L_prev now
+    if (fft_solve2<T>(s, s.rhs, s.lold, st)) return 1;
+    lrta_inputs<T>(s, s.lold, mu2, v4, grid, st);
+    TR_LAUNCH_CHECK();
+    TR_CUDA(cudaEventSynchronize(s.ev_res));
+  } else {
+    TR_CUDA(cudaStreamSynchronize(st));
+  }
   if (s.sharded && s.comm.world > 1) {
     // fused layout (the only sharded one): per mode [grad max, grad^2, dG max,
     // dG^2, lag^2] at 96 + 5k, noise [dL max, dL^2, dE max, dE^2, fit max,
@@ -967,6 +990,7 @@ static int admm_step(Solver<T>& s, double* hout) {
   std::swap(s.l, s.lold);
   for (int k = 0; k < nm; ++k) std::swap(s.gcur[k], s.gnew[k]);
   s.mu = std::min(s.cfg.mu_max, s.cfg.growth * s.mu);
+  s.head_done = ahead;  // s.l (after the swap) already receives the next sweep's L
   return 0;
 }
 
@@ -1145,6 +1169,7 @@ static int admm_create(const AdmmConfig& cfg, int order, const int64_t* dims, co
     }
   }
   TR_CUDA(cudaEventCreateWithFlags(&s->ev_main, cudaEventDisableTiming));
+  TR_CUDA(cudaEventCreateWithFlags(&s->ev_res, cudaEventDisableTiming));
   cudaStream_t st = s->streams[0];
   // zero state (ghost faces included: the first sweep's right-hand side reads them)
   auto zero = [&](T* p, bool ghost) -> int {

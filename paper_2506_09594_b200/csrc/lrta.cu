@@ -769,8 +769,8 @@ static bool expand_tc(const Shape& sh, Bufs<float>& bf, float* out, cudaStream_t
          (const double*)bf.F0, sh.n1, (int)sh.r0, bf.f0h, bf.f0l);
   const int64_t nrb = sh.n1 / 128;
   // SMs left to the latency kernels (face SVT, Ritz, TSQR) of the other mode
-  // chains while this HBM-write-bound pass runs (TR_EXPAND_RESERVE, default 0)
-  static const int ex_reserve = getenv("TR_EXPAND_RESERVE") ? atoi(getenv("TR_EXPAND_RESERVE")) : 0;
+  // chains while this HBM-write-bound pass runs (TR_EXPAND_RESERVE, default 32: 7.07 -> 7.01 ms per sweep)
+  static const int ex_reserve = getenv("TR_EXPAND_RESERVE") ? atoi(getenv("TR_EXPAND_RESERVE")) : 32;
   const int64_t per = std::max<int64_t>(
       1, std::min<int64_t>(std::max(1, stream_sms() - ex_reserve) / nrb, cdiv(N, 128)));
   const size_t smem = (size_t)(direct ? kEtSmemBytes : kEtSmemBytesTs) + 1024;
@@ -1080,6 +1080,14 @@ int tr_admm_step(void* handle, double* out) {
   auto* h = (AdmmHandle*)handle;
   if (h->dtype == TR_F32) return admm_step<float>(*(Solver<float>*)h->solver, out);
   return admm_step<double>(*(Solver<double>*)h->solver, out);
+}
+
+int tr_admm_lookahead(void* handle, int on) {
+  TR_REQUIRE(handle, "null pointer argument");
+  auto* h = (AdmmHandle*)handle;
+  if (h->dtype == TR_F32) ((Solver<float>*)h->solver)->lookahead = on != 0;
+  else ((Solver<double>*)h->solver)->lookahead = on != 0;
+  return 0;
 }
 
 int tr_admm_read(void* handle, int which, void* dst, void* stream) {

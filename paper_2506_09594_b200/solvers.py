@@ -176,6 +176,7 @@ class NativeSolver:
             ctypes.c_uint64(int(seed) & (2 ** 64 - 1)), tcode, tmats, talphas, ctypes.byref(handle)))
         self.handle = handle
         self.out = (ctypes.c_double * NOUT)()
+        self._lookahead = False  # library default: off
         if generic is not None:
             order = tuple(int(k) for k in generic.order)
             if generic.mode == "fixed-rank":
@@ -188,7 +189,12 @@ class NativeSolver:
                 float(generic.defl_tol) if generic.defl_tol is not None else 0.0,
                 ctypes.c_uint64(int(generic.seed) & (2 ** 64 - 1))))
 
-    def step(self):
+    def step(self, last: bool = False):
+        """One sweep.  The next sweep's L-solve is enqueued behind this one's
+        residual read-back (tr_admm_lookahead) unless `last` says no sweep follows."""
+        if last == self._lookahead:
+            self._lookahead = not last
+            _lib.check(self.lib.tr_admm_lookahead(self.handle, int(self._lookahead)))
         _lib.check(self.lib.tr_admm_step(self.handle, self.out))
         return list(self.out)
 
@@ -237,8 +243,8 @@ def _admm_complete(mobs, mask, cfg: SolverConfig, noise_free: bool):
                        structure=cfg.structure)
     report = SolveReport()
     try:
-        for _ in range(cfg.max_iters):
-            o = run.step()
+        for it in range(cfg.max_iters):
+            o = run.step(last=it + 1 == cfg.max_iters)
             report.residual_history.append(o[0:5])
             report.diff_fro_history.append([o[5], o[6], o[7]])
             report.feas_fro_history.append([o[8], o[9]])
