@@ -637,8 +637,12 @@ static int low_rank_step(Solver<T>& s, double tau, F&& on_main, bool main_after_
   TR_CUDA(cudaEventRecord(s.ev_main, s.streams[0]));
   for (int k = 0; k < s.cfg.nmodes; ++k) {
     cudaStream_t sk = serial ? s.streams[0] : s.streams[k + 1];
-    TR_CUDA(cudaStreamWaitEvent(sk, s.ev_main, 0));
     int rc;
+    // the fused randomized t-SVT takes the dependency on the main stream itself,
+    // after its data-independent prologue (input_ready in lrta.cu)
+    const bool defer = !s.generic && s.cfg.randomized;
+    if (defer) tl_input_ready = s.ev_main;
+    else TR_CUDA(cudaStreamWaitEvent(sk, s.ev_main, 0));
     if (s.generic)
       rc = generic_svt<T>(s, s.X[k], s.gnew[k], tau, sk);
     else if (s.cfg.randomized)
@@ -648,6 +652,10 @@ static int low_rank_step(Solver<T>& s, double tau, F&& on_main, bool main_after_
                                    !s.tf_built.empty() && s.tf_built[k]);
     else
       rc = full_svt<T>(s, s.X[k], s.gnew[k], tau, s.ws[k], sk);
+    if (tl_input_ready) {  // never consumed (error path): keep the order anyway
+      cudaStreamWaitEvent(sk, tl_input_ready, 0);
+      tl_input_ready = nullptr;
+    }
     if (rc) return rc;
     if (!s.generic && s.cfg.randomized) {
       if (s.tf_built.empty()) s.tf_built.assign(s.cfg.nmodes, 0);

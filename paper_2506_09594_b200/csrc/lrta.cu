@@ -29,6 +29,18 @@ void set_error(const char* fmt, ...) {
   va_end(ap);
 }
 
+// Deferred input dependency of a t-SVT (set by the ADMM solver): the stream
+// waits for this event right before its first kernel that reads the input
+// tensor, so the data-independent prologue (ticket reset, Philox sketch rows)
+// runs while the producer of the input is still busy on another stream.
+static thread_local cudaEvent_t tl_input_ready = nullptr;
+static inline void input_ready(cudaStream_t st) {
+  if (tl_input_ready) {
+    cudaStreamWaitEvent(st, tl_input_ready, 0);
+    tl_input_ready = nullptr;
+  }
+}
+
 // Bump allocator over the caller's workspace; base == nullptr only sizes.
 struct Carve {
   char* base;
@@ -306,6 +318,7 @@ static int64_t panel_mma(const float* A, int64_t m, int64_t n, int b, const floa
              (unsigned)std::min<int64_t>(cdiv(total, 128), 8 * num_sms()), 128, 0, st, n, bw, sk,
              gover, rows, j0, b);
     }
+    input_ready(st);  // everything before this line is independent of A
     const float* cf = MODE == 0 ? rows : nullptr;
     const float* Pj = MODE == 1 ? P + m * (int64_t)j0 : P;
     np = m <= 512    ? panel_mma_launch<1, MODE, 1>(A, Pj, cf, pa, partial, st)
@@ -326,6 +339,7 @@ static int64_t panel(const T* A, int64_t m, int64_t n, int b, const T* P, const 
                      SketchSpec sk, T* rows, double* partial, cudaStream_t st) {
   const int64_t np = panel_mma<MODE>(A, m, n, b, P, gover, sk, rows, partial, st);
   if (np >= 0) return np;
+  input_ready(st);
   PanelArgs pa;
   pa.m = m;
   pa.n = n;
@@ -520,8 +534,10 @@ static int bki_mode(const Shape& sh, const T* A, int64_t m, int64_t n, int r, in
     launch("normalize_piece", k_normalize_piece<T>, 1, 1024, 0, st, slot, m * b, bf.P);
     return 0;
   };
+  if (!fused) input_ready(st);
   int64_t np = fused ? panel<T, 0>(A, m, n, b, nullptr, gover, sk, bf.coef, bf.partial, st)
                      : rank_update<T>(A, m, n, b, nullptr, gover, sk, bf.partial, st);
+  input_ready(st);  // (no-op: the sketch pass has consumed it)
   if (reduce_normalize(np, bf.K)) return 1;
   for (int k = 1; k <= q; ++k) {
     if (fused) {
