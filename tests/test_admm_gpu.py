@@ -172,3 +172,36 @@ def test_deterministic_large_faces_match_oracle(cuda_lib):
     # the fp32 stream through the same large-face path
     l32, e32, _ = pk.gnrhtc(mobs.astype(np.float32), mask, pk.SolverConfig(max_iters=4))
     assert np.linalg.norm(l32 - lo) / np.linalg.norm(lo) <= 1e-4
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_lookahead_is_bit_identical(cuda_lib, dtype):
+    """tr_admm_lookahead only moves the next sweep's L-solve ahead of the host's
+    read-back: residual histories, L and E must not change by a bit, whether the
+    loop runs to max_iters or stops early with a lookahead in flight."""
+    import paper_2506_09594_b200 as pk
+    from paper_2506_09594_b200.solvers import NativeSolver
+    from paper_2506_09594_b200.tensors import from_device, mask_to_device, to_device
+
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((32, 16, 3)) @ rng.standard_normal((3, 24))
+    x = np.moveaxis(x, 1, 2).astype(dtype)  # 32 x 24 x 16, low rank along mode 1
+    x = np.asfortranarray(x + 0.01 * rng.standard_normal(x.shape).astype(dtype))
+    mask = rng.random(x.shape) < 0.6
+    sk = pk.SketchConfig(mode="fixed-rank", order=(0, 1), ranks=(6, 6), blocks=(3, 3),
+                         krylov=(2, 2), seed=11)
+    cfg = pk.SolverConfig(phi=pk.MCP(2.5), psi=pk.MCP(2.5), randomized=True, sketch=sk, tol=1e-30)
+
+    def run(lookahead, sweeps):
+        cm = to_device(x * mask)
+        s = NativeSolver("gnrhtc", cm, None, mask_to_device(mask), cfg, cfg.device_modes(x.shape),
+                         cfg.lam_for(x.shape))
+        hist = [s.step(last=not lookahead) for _ in range(sweeps)]
+        out = from_device(s.read(0)).copy(), from_device(s.read(1)).copy()
+        s.close()
+        return np.array(hist), out
+
+    h0, (l0, e0) = run(False, 7)
+    h1, (l1, e1) = run(True, 7)   # stops with the 8th sweep's L-solve enqueued
+    assert np.array_equal(h0, h1)
+    assert np.array_equal(l0, l1) and np.array_equal(e0, e1)
