@@ -55,8 +55,10 @@ static void run(const char* name, Geom g, std::vector<float*>& buf, uint8_t* mas
          bytes / (best * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
 }
 
-int main() {
-  const int64_t dims[3] = {1024, 1024, 128};
+int main(int argc, char** argv) {
+  // default: the bench geometry; "tail_probe 512 512 512" exercises the short-line walk
+  const int64_t dims[3] = {argc > 3 ? atoll(argv[1]) : 1024, argc > 3 ? atoll(argv[2]) : 1024,
+                           argc > 3 ? atoll(argv[3]) : 128};
   Geom g{};
   g.d = 3;
   g.N = 1;
