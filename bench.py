@@ -21,7 +21,14 @@ blocks / Ritz Gram / core, shard.py); ``--step admm-sharded`` times one GNRHTC
 sweep of BASELINE configs[4]'s tensor sharded along its last mode (global
 2048x2048x32x(4N), 4 faces per rank: exactly configs[4] at N = 8; weak
 scaling; all-to-all FFT transpose, halo exchanges, sharded t-SVTs).  Every
-tensor is 512 MB (> 126 MB L2), so no explicit flush is needed.
+tensor is 512 MB (> 126 MB L2), so no explicit flush is needed.  The solver
+runs with its lookahead on, as the public solvers do (the next sweep's L-solve
+is enqueued before the host reads a sweep's residuals): the timed region of K
+steps holds exactly K L-solves and K of everything else (the first step's
+L-solve was enqueued by the last warm-up step, the K-th step enqueues the next).
+The ``roofline`` object is the kernel category with the largest UNCONTENDED
+device time per step (the three t-SVT chains of a sweep overlap on concurrent
+streams, so their categories are timed in a standalone t-SVT pass).
 
 Multi-GPU: one process per GPU (torchrun); each rank solves its own problem
 (independent recoveries, weak scaling, no data-path collective); time = max
