@@ -289,7 +289,9 @@ def run_ours(args):
     local = _env_int("LOCAL_RANK", 0)
     torch.cuda.set_device(local)
     sharded = args.step == "tsvt-sharded"
-    if world > 1:
+    # under torchrun (any world size, 1 included) the rendezvous comes from its
+    # environment: an explicit tcp:// store would wait for the agent's store
+    if world > 1 or "TORCHELASTIC_RUN_ID" in os.environ:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     elif sharded:  # a one-rank NCCL group for the same code path
         import socket
@@ -542,7 +544,7 @@ def run_ours(args):
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args.step, full=args.step == "admm")
         print(json.dumps(line), flush=True)
-    if world > 1 or sharded:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 
@@ -1014,7 +1016,7 @@ def run_admm_sharded(args):
     rank = _env_int("RANK", 0)
     local = _env_int("LOCAL_RANK", 0)
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or "TORCHELASTIC_RUN_ID" in os.environ:  # torchrun: its own rendezvous
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         import socket
